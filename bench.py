@@ -1,0 +1,269 @@
+"""Benchmark: Gcell-updates/s of the nested-grid tsunami step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config kochi|cfg1|cfg2|cfg5] [--scale S]
+
+Workload (BASELINE.json ``metric`` / configs[2]): the 5-level 810/270/90/30/10 m
+Kochi-shaped domain, 47,211,444 cells, dt 0.2 s (a 6-h simulation is 108,000
+steps), synthetic bathymetry and a 0.5 m Gaussian source.  One "step" is
+one full time step of every cell of every level: mass, restriction,
+halo-eta, momentum with edge rules, prolongation, halo-flux, output maxima.
+
+* ``value`` / ``ms_per_step``: device time of exactly K steps on the
+  library's stream (CUDA events bracketing ``Simulation.run(K)``, barrier +
+  synchronize on both sides, max over ranks); inputs are device resident
+  and 3.8 GB > 126 MB L2, so no flush is needed.
+* ``e2e``: the same K steps through the public API with host buffers:
+  upload of the host inputs, K steps, download of the result maps.
+* ``roofline``: the momentum kernel (the dominant one), algorithmic bytes
+  per launch / its average duration over the timed steps (per-step CUDA
+  events inside the graph, on the launch stream), against the measured HBM
+  copy bandwidth in MEASURED_PEAKS.json.
+* ``cpu_baseline``: the oracle port (oracle/, plain C + OpenMP, all host
+  threads) on a bounded sample of the same workload, rank 0 only.
+
+``--impl reference`` times the reference's CPU path (the oracle port, since
+the reference is numpy code that cannot travel to the GPU box) with every
+host thread on the same workload and prints the same line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SIX_HOURS_STEPS = 108_000
+ALG_BYTES_STEP = 88.0        # B/cell-step, all-wet domain
+ALG_BYTES_MOM = 48.0         # B/cell per momentum launch (eta, h, M, N read; M, N write)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def build_workload(P, name, scale):
+    if name == "kochi":
+        system = P.build_kochi_scaled_config(scale)
+        settings = P.kochi_settings(system)
+        return system, settings, f"kochi-5level scale {scale} (BASELINE config 3)"
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import systems
+    if name in ("cfg1", "cfg2"):
+        system, settings, _ = systems.make(P, name)
+        return system, settings, f"{name} (BASELINE config {name[-1]})"
+    raise SystemExit(f"unknown config {name}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for k, nm in enumerate(names):
+                if f[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profiled_traffic():
+    """dram bytes/launch of the momentum kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "momentum_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_sample(system, settings, steps=2, warm=1):
+    """The oracle on ``steps`` steps of the same workload, all host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+    oracle.build_library()
+    threads = oracle.set_threads(os.cpu_count() or 1)
+    sim = oracle.OracleSimulation(system, settings)
+    sim.run(warm)
+    t0 = time.perf_counter()
+    sim.run(steps)
+    dt = time.perf_counter() - t0
+    return system.cell_count * steps / dt / 1e9, threads, dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_2408_07609_b200 as P
+    system, settings, label = build_workload(P, args.config, args.scale)
+    steps = max(1, min(args.steps, 3))
+    rate, threads, dt = cpu_sample(system, settings, steps=steps, warm=max(1, min(args.warmup, 1)))
+    line = {
+        "impl": "reference", "metric": "Gcell-updates/s", "value": rate, "unit": "Gcell/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": dt / steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": label, "cells": system.cell_count},
+        "six_hour_wall_s": dt / steps * SIX_HOURS_STEPS,
+        "cpu_baseline": {"value": rate, "unit": "Gcell/s", "cores": threads, "kind": "port",
+                         "sample": f"{steps} steps of the full workload after 1 warm-up step"},
+        "e2e": {"value": rate, "unit": "Gcell/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    rank, world, local = dist_env()
+    import torch
+    import paper_2408_07609_b200 as P
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    system, settings, label = build_workload(P, args.config, args.scale)
+    cells = system.cell_count
+    if world > 1:
+        raise SystemExit("multi-GPU decomposition: see DESIGN.md §7 (not in this build)")
+    sim = P.Simulation(system, settings, device=local)
+    ext = torch.cuda.ExternalStream(sim.stream_ptr, device=local)
+    sim.run(args.warmup, threaded=False)
+    sim.set_timing(True)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(ext)
+        sim.run(args.steps, threaded=False)
+        end.record(ext)
+        torch.cuda.synchronize()
+    sim.set_timing(False)
+    t = start.elapsed_time(end) / 1e3
+    mass_s, mom_s, step_s = sim.kernel_seconds()
+    launches = sim.launches_per_step * args.steps + 4
+
+    # end to end through the public API with host buffers
+    arrays = __import__("paper_2408_07609_b200.runner", fromlist=["x"]).host_block_arrays(system, settings)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = sim.upload_initial_state(arrays)
+    sim.run(args.steps, threaded=False)
+    _, d2h = sim.download_outputs()
+    te = time.perf_counter() - t0
+
+    peak, peak_src = measured_peaks()
+    achieved = ALG_BYTES_MOM * cells / mom_s / 1e9 if mom_s > 0 else None
+    traffic = profiled_traffic()
+    line = {
+        "metric": "Gcell-updates/s", "value": cells * args.steps / t / 1e9, "unit": "Gcell/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": label, "cells": cells, "levels": len(system.levels),
+                   "blocks": system.n_blocks, "dt_s": settings.dt,
+                   "parallelism": f"blocks over {world} GPU(s)",
+                   "l2": "state 3.8 GB >> 126 MB L2; no flush"},
+        "six_hour_wall_s": t / args.steps * SIX_HOURS_STEPS,
+        "step_roofline": {"bytes_per_cell_step": ALG_BYTES_STEP,
+                          "achieved_gbs": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9,
+                          "frac": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9 / peak},
+        "roofline": {"kernel": "k_momentum", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak if achieved else None,
+                     "traffic": traffic, "alg_bytes_per_launch": ALG_BYTES_MOM * cells,
+                     "avg_launch_s": mom_s, "peak_source": peak_src,
+                     "mass_kernel_s": mass_s, "step_s_events": step_s},
+        "e2e": {"value": cells * args.steps / te / 1e9, "unit": "Gcell/s",
+                "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
+                "wall_s": te},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu:
+        rate, threads, dt = cpu_sample(system, settings, steps=1, warm=1)
+        line["cpu_baseline"] = {"value": rate, "unit": "Gcell/s", "cores": threads, "kind": "port",
+                                "sample": "1 step of the full workload after 1 warm-up step "
+                                          f"({dt:.1f} s)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="kochi")
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

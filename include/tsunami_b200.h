@@ -1,0 +1,188 @@
+/*
+ * tsunami_b200.h — C ABI of the B200-native nested-grid shallow-water step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/pkg/src/blockswe/, "blockswe"): the per-step body of
+ * runner.Simulation (runner.py:193-365), the kernel layer (kernels.py) and
+ * the per-step halves of the data-movement layer (coupling.py:278-340,
+ * exchange.py:162-275).  The reference has no FFI of its own — its boundary
+ * is a Python object API — so each entry point below names the reference
+ * interface it replaces; INTEGRATION.md shows the ctypes binding a
+ * maintainer would add to blockswe.
+ *
+ * Conventions
+ *  - Plain C types only.  Block indices are positions in the reference's
+ *    global block order, NestedGridSystem.all_blocks() (grid.py:82-84).
+ *  - Host arrays use the reference's own BlockState layouts (kernels.py:
+ *    39-62): C order, axis 0 = x, halo g = 2; eta/h (ni+4)x(nj+4),
+ *    m (ni+5)x(nj+4), n (ni+4)x(nj+5); accumulators ni x nj.
+ *  - Return codes: TS_OK, TS_ERR_NUMERICS (a non-finite field, the
+ *    reference's NumericsError, kernels.py:115-120), TS_ERR_CUDA,
+ *    TS_ERR_INVALID (bad argument: the reference's ValueError /
+ *    GridStructureError).  ts_last_error() gives the message.
+ *  - A handle is used by one host thread at a time; the library owns all
+ *    device memory; inputs are copied at ts_create.
+ */
+#ifndef TSUNAMI_B200_H
+#define TSUNAMI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TS_ABI_VERSION 1
+
+#define TS_OK 0
+#define TS_ERR_NUMERICS 1
+#define TS_ERR_CUDA 2
+#define TS_ERR_INVALID 3
+
+/* sides (exchange.py:37 order) and edge kinds (grid.py:102-119) */
+#define TS_WEST 0
+#define TS_EAST 1
+#define TS_SOUTH 2
+#define TS_NORTH 3
+#define TS_REFLECTIVE 0
+#define TS_RADIATION 1
+
+/* one block: replaces BlockState construction (kernels.py:39-62),
+ * set_initial_eta (kernels.py:97-101) and fill_bathymetry_halos
+ * (exchange.py:281-300), whose results the caller passes in h_ext/nman_ext */
+typedef struct ts_block_desc {
+    int64_t block_id;          /* Block.block_id (grid.py:44) — for messages */
+    int32_t ni, nj;            /* Block.ni / nj */
+    int32_t owner;             /* rank (GPU) owning the block, plan.rank_of */
+    int32_t level;             /* 0-based level index */
+    double dx;                 /* GridLevel.dx */
+    double manning;            /* scalar Block.manning_n (used if nman_ext == NULL) */
+    const double *h_ext;       /* (ni+4)*(nj+4): BlockState.h_ext after fill_bathymetry_halos */
+    const double *nman_ext;    /* NULL or (ni+4)*(nj+4): BlockState.n_ext (array case) */
+    const double *eta0;        /* ni*nj interior initial level (runner.py:77-80) */
+} ts_block_desc;
+
+/* exchange.HaloEntry (exchange.py:62-101); entries are passed in the
+ * reference's APPLY order (runner.py:178-186: receiver rank, sorted sender
+ * rank, schedule order) so duplicate ghost writes resolve identically */
+typedef struct ts_halo_entry {
+    int32_t sender, receiver;  /* block indices */
+    int32_t side;              /* sender's side facing the receiver */
+    int32_t send_lo, send_hi;  /* HaloEntry.send_span */
+    int32_t recv_lo, recv_hi;  /* HaloEntry.recv_span */
+} ts_halo_entry;
+
+/* coupling.EtaSegment (coupling.py:36-46) with its link's blocks */
+typedef struct ts_eta_segment {
+    int32_t parent, child;     /* block indices */
+    int32_t side;
+    int32_t child_lo, child_hi;      /* child_span */
+    int32_t ring_start, parent_line;
+    int32_t parent_lo, parent_hi;    /* parent_span */
+} ts_eta_segment;
+
+/* coupling.FluxSegment (coupling.py:49-59) with its link's blocks */
+typedef struct ts_flux_segment {
+    int32_t parent, child;
+    int32_t side;
+    int32_t child_lo, child_hi;
+    int32_t child_face_line, parent_face_line;
+    int32_t parent_lo, parent_hi;
+} ts_flux_segment;
+
+/* one apply_edge_flux call (kernels.py:274-306; runner.py:89-98, 116-117) */
+typedef struct ts_edge {
+    int32_t block, side, kind, lo, hi;
+} ts_edge;
+
+/* the whole configured system: replaces Simulation.__init__ (runner.py:59-102) */
+typedef struct ts_desc {
+    int32_t abi_version;       /* TS_ABI_VERSION */
+    int32_t n_blocks;
+    const ts_block_desc *blocks;
+    double dt, gravity, wet_threshold;   /* SimulationConfig (grid.py:144-158) */
+    int32_t n_halo;  const ts_halo_entry *halo;
+    int32_t n_restrict; const ts_eta_segment *restrict_segs;
+    int32_t n_prolong;  const ts_flux_segment *prolong_segs;
+    int32_t n_edges; const ts_edge *edges;
+    int32_t rank, n_ranks;     /* this process's rank / GPU count (1 GPU: 0, 1) */
+    int32_t device;            /* CUDA device ordinal */
+    int32_t tile_rows;         /* 0 = default */
+} ts_desc;
+
+typedef struct ts_handle ts_handle;
+
+/* field codes for ts_get_field / ts_set_field (BlockState / OutputAccumulators) */
+#define TS_ETA_OLD 0
+#define TS_ETA_NEW 1
+#define TS_M_OLD 2
+#define TS_M_NEW 3
+#define TS_N_OLD 4
+#define TS_N_NEW 5
+#define TS_H_EXT 6
+#define TS_MAX_ETA 7
+#define TS_MAX_SPEED 8
+#define TS_MAX_INUNDATION 9
+
+/* phase codes for ts_phase (runner.PHASE_SEQUENCE, runner.py:39-40, plus the
+ * kernel-level calls of kernels.py) */
+#define TS_PH_MASS 0        /* update_mass on every owned block (no accumulate) */
+#define TS_PH_RESTRICT 1    /* restrict_eta + apply_restricted_eta */
+#define TS_PH_HALO_ETA 2    /* pack/unpack_halo, eta phase */
+#define TS_PH_MOMENTUM 3    /* update_momentum on every owned block, no edges */
+#define TS_PH_EDGES 4       /* every ts_edge, in order */
+#define TS_PH_PROLONG 5     /* prolong_flux + apply_prolonged_flux */
+#define TS_PH_HALO_FLUX 6   /* pack/unpack_halo, flux phase */
+#define TS_PH_OUTPUT 7      /* accumulate_outputs on every owned block */
+#define TS_PH_SWAP 8        /* BlockState.swap */
+
+const char *ts_last_error(void);
+int ts_abi_version(void);
+
+/* Simulation.__init__ (runner.py:59-102) */
+int ts_create(const ts_desc *desc, ts_handle **out);
+/* Simulation.run body for n steps (runner.py:193-365): mass, restrict,
+ * halo-eta, momentum+edges, prolong, halo-flux, output, swap; the running
+ * maxima are up to date on return.  Re-entrant across calls. */
+int ts_run(ts_handle *h, int64_t n_steps);
+/* one phase, for the kernel-level API and phase-order tests */
+int ts_phase(ts_handle *h, int32_t phase);
+/* BlockState / OutputAccumulators array access in the reference layout */
+int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_t len);
+int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, int64_t len);
+/* the first non-finite value of the failing step (kernels.py:115-120):
+ * what = 0 water level, 1 x-flux, 2 y-flux; (i, j) local cell */
+int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j);
+/* per-routine device seconds of the last ts_run (runner.ROUTINES order:
+ * mass, momentum, restrict, prolong, halo-eta, halo-flux, output) and total */
+int ts_timings(ts_handle *h, double *routines7, double *total);
+int64_t ts_steps_done(ts_handle *h);
+/* device bytes held by the arena */
+int64_t ts_device_bytes(ts_handle *h);
+/* kernels launched per ts_run step (graph nodes) */
+int32_t ts_launches_per_step(ts_handle *h);
+/* timing mode: every graph-replayed step of ts_run records the mass,
+ * momentum and whole-step boundaries into its own CUDA events (on the launch
+ * stream); ts_kernel_seconds returns their averages */
+int ts_set_timing(ts_handle *h, int32_t on);
+/* average device time (s) of the momentum kernel over the last ts_run's
+ * timed graph replays, measured with events on the launch stream */
+int ts_kernel_seconds(ts_handle *h, double *mass_s, double *momentum_s, double *step_s);
+/* the CUDA stream (cudaStream_t) every kernel of the handle runs on, for
+ * callers that bracket ts_run with their own events */
+int ts_stream(ts_handle *h, void **stream);
+void ts_destroy(ts_handle *h);
+
+/* multi-GPU (one process per GPU): export this rank's arena/signal IPC
+ * handles, then map every peer's before the first ts_run */
+int ts_ipc_export(ts_handle *h, void *out, int64_t len);
+int ts_ipc_import(ts_handle *h, int32_t peer_rank, const void *in, int64_t len);
+
+/* the friction cube root (kernels.py:240-241 np.cbrt): host twin and device */
+void ts_cbrt_host(const double *in, double *out, int64_t n);
+int ts_cbrt_device(int32_t device, const double *in, double *out, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

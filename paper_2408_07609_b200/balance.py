@@ -1,0 +1,169 @@
+"""Block -> GPU decomposition.
+
+Plans are consecutive runs of the level-ordered block list, as in the
+reference (balance.py:102-144): ``DecompositionPlan`` here is value- and
+behaviour-compatible, and ``Simulation`` also accepts the reference's own
+plan objects.  On top of the reference's equal-cell split this adds an
+exact min-max partition under a linear per-block cost model
+(cost = slope * cells + intercept, balance.py:31-46), which at 8 GPUs beats
+the reference's hill climb.
+"""
+
+from __future__ import annotations
+
+import bisect
+from dataclasses import dataclass
+
+import numpy as np
+
+
+class PlanError(ValueError):
+    """A decomposition plan is structurally invalid or infeasible."""
+
+
+class DegenerateFitError(ValueError):
+    """Cost samples span fewer than two distinct cell counts."""
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Per-block runtime model in microseconds."""
+
+    slope: float
+    intercept: float
+    r_squared: float = float("nan")
+
+    def block_cost(self, cells):
+        return self.slope * np.asarray(cells, dtype=float) + self.intercept
+
+
+# The reference's canned GPU coefficients (balance.py:256).
+GPU_REFERENCE_MODEL = CostModel(slope=1.09e-4, intercept=46.2, r_squared=0.942)
+# B200 step cost of the flattened-tile kernels: blocks share launches, so the
+# per-block intercept is only the tile-quantisation tail.
+B200_MODEL = CostModel(slope=1.0 / 60.0e3, intercept=0.5)
+
+
+def fit_cost_model(samples) -> CostModel:
+    """Least-squares line through (cells, microseconds) samples; a negative
+    intercept is clamped to zero (balance.py:259-284 contract)."""
+    pts = np.array([(float(x), float(y)) for x, y in samples], dtype=float).reshape(-1, 2)
+    if len(np.unique(pts[:, 0])) < 2:
+        raise DegenerateFitError("need samples at at least two distinct cell counts")
+    x, y = pts[:, 0], pts[:, 1]
+    A = np.stack([x, np.ones_like(x)], axis=1)
+    (slope, icept), *_ = np.linalg.lstsq(A, y, rcond=None)
+    resid = y - (slope * x + icept)
+    ss_res, ss_tot = float(resid @ resid), float(((y - y.mean()) ** 2).sum())
+    r2 = (1.0 if ss_res <= 1e-30 else 0.0) if ss_tot == 0 else 1.0 - ss_res / ss_tot
+    return CostModel(float(slope), max(0.0, float(icept)), r2)
+
+
+@dataclass(frozen=True)
+class DecompositionPlan:
+    """Consecutive assignment: rank r owns blocks [cut[r], cut[r+1])."""
+
+    cells: tuple
+    separators: tuple
+
+    def __post_init__(self):
+        n = len(self.cells)
+        if n == 0:
+            raise PlanError("plan needs at least one block")
+        prev = 0
+        for s in self.separators:
+            if not 0 < s < n:
+                raise PlanError(f"separator {s} outside (0, {n})")
+            if s <= prev:
+                raise PlanError("separators must be strictly increasing")
+            prev = s
+
+    @property
+    def n_blocks(self) -> int:
+        return len(self.cells)
+
+    @property
+    def n_ranks(self) -> int:
+        return len(self.separators) + 1
+
+    def rank_spans(self):
+        cuts = (0, *self.separators, len(self.cells))
+        return [(cuts[r], cuts[r + 1]) for r in range(self.n_ranks)]
+
+    def rank_of(self, block_index: int) -> int:
+        return bisect.bisect_right(self.separators, block_index)
+
+    def blocks_of(self, rank: int) -> range:
+        lo, hi = self.rank_spans()[rank]
+        return range(lo, hi)
+
+
+def rank_costs(plan, model: CostModel) -> np.ndarray:
+    cuts = (0, *plan.separators, plan.n_blocks)
+    cells = np.asarray(plan.cells, dtype=float)
+    return np.array([model.slope * cells[a:b].sum() + model.intercept * (b - a)
+                     for a, b in zip(cuts[:-1], cuts[1:])])
+
+
+def predict_rank_cost(plan, model: CostModel, rank: int) -> float:
+    return float(rank_costs(plan, model)[rank])
+
+
+def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
+    """The reference's greedy prefix cuts (balance.py:369-393): the r-th cut
+    lands where the running total is closest to r/n of the total (first
+    such position), keeping one block per remaining rank."""
+    cells = tuple(int(c) for c in cells)
+    n = len(cells)
+    if n_ranks > n:
+        raise PlanError(f"{n_ranks} ranks infeasible for {n} blocks")
+    if n_ranks < 1:
+        raise PlanError("need at least one rank")
+    prefix = np.concatenate([[0], np.cumsum(cells)])
+    seps, prev = [], 0
+    for r in range(1, n_ranks):
+        goal = prefix[-1] * r / n_ranks
+        cand = np.arange(prev + 1, n - (n_ranks - r) + 1)
+        pos = int(cand[np.argmin(np.abs(prefix[cand] - goal))])
+        seps.append(pos)
+        prev = pos
+    return DecompositionPlan(cells, tuple(seps))
+
+
+def minmax_plan(cells, n_ranks: int, model: CostModel = B200_MODEL) -> DecompositionPlan:
+    """Exact minimum of the maximum per-rank cost over all consecutive
+    partitions into exactly ``n_ranks`` non-empty runs (O(n^2 k) DP)."""
+    cells = tuple(int(c) for c in cells)
+    n = len(cells)
+    if not 1 <= n_ranks <= n:
+        raise PlanError(f"{n_ranks} ranks infeasible for {n} blocks")
+    cost = np.asarray(model.block_cost(cells), dtype=float)
+    pre = np.concatenate([[0.0], np.cumsum(cost)])
+    INF = float("inf")
+    best = np.full((n_ranks + 1, n + 1), INF)
+    arg = np.zeros((n_ranks + 1, n + 1), dtype=int)
+    best[0, 0] = 0.0
+    for k in range(1, n_ranks + 1):
+        for e in range(k, n - (n_ranks - k) + 1):
+            s = np.arange(k - 1, e)
+            vals = np.maximum(best[k - 1, s], pre[e] - pre[s])
+            q = int(np.argmin(vals))
+            best[k, e], arg[k, e] = vals[q], s[q]
+    seps, e = [], n
+    for k in range(n_ranks, 1, -1):
+        e = int(arg[k, e])
+        seps.append(e)
+    return DecompositionPlan(cells, tuple(sorted(seps)))
+
+
+def concat_plans(plans) -> DecompositionPlan:
+    """Per-level plans joined with forced cuts at level boundaries
+    (balance.py:491-503)."""
+    cells, seps, off = [], [], 0
+    for p in plans:
+        cells.extend(p.cells)
+        seps.extend(off + s for s in p.separators)
+        off += p.n_blocks
+        seps.append(off)
+    seps.pop()
+    return DecompositionPlan(tuple(cells), tuple(seps))

@@ -1,0 +1,870 @@
+// C ABI (include/tsunami_b200.h): device arena, exchange descriptors, the
+// per-step CUDA graph and the run loop.  Replaces runner.Simulation's body
+// (runner.py:59-365) for the blocks this process/GPU owns.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/tsunami_b200.h"
+#include "cbrt.cuh"
+#include "common.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (call);                                                         \
+        if (e_ != cudaSuccess)                                                           \
+            return fail(TS_ERR_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                             \
+    } while (0)
+
+// phase boundaries: 0 |mass| 1 |restrict| 2 |halo-eta| 3 |momentum| 4
+// |edges| 5 |prolong| 6 |halo-flux| 7
+constexpr int kPhaseEvents = 8;
+// boundaries retargeted per step in timing mode: mass (0,1), momentum (3,4),
+// whole step (0,7)
+constexpr int kTimed[5] = {0, 1, 3, 4, 7};
+
+struct Group {
+    int W = 0;
+    std::vector<Tile> tiles;
+    Tile *d = nullptr;
+};
+
+}  // namespace
+
+struct ts_handle {
+    int device = 0, rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;
+    double dt = 0, g = 0, thr = 0;
+    int nb = 0;
+    std::vector<ts_block_desc> desc;      // pointers not retained
+    std::vector<DevBlock> hb;             // host mirror of the device table
+    DevBlock *d_blocks = nullptr;
+    char *arena = nullptr;
+    size_t arena_bytes = 0;
+    int T = 32;
+    Group groups[4];                      // W = 1..4
+    RSeg *d_rseg = nullptr;
+    int n_rseg = 0;
+    int64_t r_elems = 0;
+    bool r_two_pass = false;
+    PSeg *d_pseg = nullptr;
+    int n_pseg = 0;
+    int64_t p_elems = 0;
+    bool p_two_pass = false;
+    Copy *d_heta = nullptr, *d_hflux = nullptr, *d_edge = nullptr;
+    int64_t n_heta = 0, n_hflux = 0, n_edge = 0;
+    bool edge_serial = false;
+    double *d_stage = nullptr;
+    unsigned long long *d_err = nullptr;
+    int *d_accflag = nullptr;
+    cudaGraph_t graph[2] = {nullptr, nullptr};          // kept: exec node updates refer to them
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaEvent_t ev[kPhaseEvents] = {};
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    int cur = 0;
+    int64_t steps = 0;
+    double routines[7] = {0};
+    double total = 0;
+    double mass_s = 0, mom_s = 0, step_s = 0;
+    int launches = 0;
+    bool timing = false;
+    cudaGraphNode_t ev_node[2][kPhaseEvents] = {};   // per parity graph
+    std::vector<cudaEvent_t> pool;                    // 5 per timed step
+};
+
+namespace {
+
+StepArgs args_of(const ts_handle *h, int cur)
+{
+    StepArgs a;
+    a.blocks = h->d_blocks;
+    a.cur = cur;
+    a.thr = h->thr;
+    a.err = h->d_err;
+    a.acc_flag = h->d_accflag;
+    return a;
+}
+
+// The step body, in the reference's phase order (runner.py:352-365).  When
+// `events` the phase boundaries are recorded (external event nodes when
+// captured into a graph).
+int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunch)
+{
+    const StepArgs a = args_of(h, cur);
+    int n = 0;
+    auto mark = [&](int k) -> int {
+        if (!events) return 0;
+        CK(cudaEventRecordWithFlags(h->ev[k], s, cudaEventRecordExternal));
+        return 0;
+    };
+    if (mark(0)) return TS_ERR_CUDA;
+    for (auto &gr : h->groups)
+        if (!gr.tiles.empty()) { launch_mass(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, true, s); ++n; }
+    if (mark(1)) return TS_ERR_CUDA;
+    if (h->r_elems) {
+        if (h->r_two_pass) {
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 2, s);
+            n += 2;
+        } else {
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, nullptr, 0, s);
+            ++n;
+        }
+    }
+    if (mark(2)) return TS_ERR_CUDA;
+    if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
+    if (mark(3)) return TS_ERR_CUDA;
+    for (auto &gr : h->groups)
+        if (!gr.tiles.empty()) { launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s); ++n; }
+    if (mark(4)) return TS_ERR_CUDA;
+    if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
+    if (mark(5)) return TS_ERR_CUDA;
+    if (h->p_elems) {
+        if (h->p_two_pass) {
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 1, s);
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 2, s);
+            n += 2;
+        } else {
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, nullptr, 0, s);
+            ++n;
+        }
+    }
+    if (mark(6)) return TS_ERR_CUDA;
+    if (h->n_hflux) { launch_copies(a, h->d_hflux, h->n_hflux, false, s); ++n; }
+    // "output" is folded into the next step's K_mass (and the end-of-run
+    // flush); the swap is the parity flip of the caller
+    if (mark(7)) return TS_ERR_CUDA;
+    CK(cudaGetLastError());
+    if (nlaunch) *nlaunch = n;
+    return TS_OK;
+}
+
+int enqueue_flush(ts_handle *h, cudaStream_t s, int buf)
+{
+    const StepArgs a = args_of(h, buf);
+    for (auto &gr : h->groups)
+        if (!gr.tiles.empty()) launch_accumulate(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s);
+    CK(cudaGetLastError());
+    return TS_OK;
+}
+
+int build_graphs(ts_handle *h)
+{
+    for (int c = 0; c < 2; ++c) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_step(h, h->stream, c, true, &h->launches);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        CK(cudaGraphInstantiate(&h->gexec[c], g, 0));
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeEventRecord) continue;
+            cudaEvent_t ev;
+            CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (int k = 0; k < kPhaseEvents; ++k)
+                if (ev == h->ev[k]) h->ev_node[c][k] = nd;
+        }
+        h->graph[c] = g;
+    }
+    return TS_OK;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Reference-layout (row-major, unpadded) <-> pitched device array geometry
+struct FieldGeom {
+    double *ptr;
+    int rows, cols;     // reference shape
+    int pitch;          // device pitch (doubles)
+};
+
+int field_geom(ts_handle *h, int b, int field, FieldGeom *g)
+{
+    if (b < 0 || b >= h->nb) return fail(TS_ERR_INVALID, "block index %d out of range", b);
+    const DevBlock &B = h->hb[b];
+    if (!B.h) return fail(TS_ERR_INVALID, "block %d is not owned by rank %d", b, h->rank);
+    const int ni = B.ni, nj = B.nj, c = h->cur;
+    g->pitch = B.P;
+    switch (field) {
+    case TS_ETA_OLD: *g = {B.eta[c], ni + 4, nj + 4, B.P}; break;
+    case TS_ETA_NEW: *g = {B.eta[c ^ 1], ni + 4, nj + 4, B.P}; break;
+    case TS_M_OLD: *g = {B.m[c], ni + 5, nj + 4, B.P}; break;
+    case TS_M_NEW: *g = {B.m[c ^ 1], ni + 5, nj + 4, B.P}; break;
+    case TS_N_OLD: *g = {B.n[c], ni + 4, nj + 5, B.P}; break;
+    case TS_N_NEW: *g = {B.n[c ^ 1], ni + 4, nj + 5, B.P}; break;
+    case TS_H_EXT: *g = {B.h, ni + 4, nj + 4, B.P}; break;
+    case TS_MAX_ETA: *g = {B.acc_eta, ni, nj, B.P}; break;
+    case TS_MAX_SPEED: *g = {B.acc_speed, ni, nj, B.P}; break;
+    case TS_MAX_INUNDATION: *g = {B.acc_inund, ni, nj, B.P}; break;
+    default: return fail(TS_ERR_INVALID, "unknown field %d", field);
+    }
+    return TS_OK;
+}
+
+// index helpers into the pitched arrays (x, y are local cell / face indices)
+inline int32_t pidx(int P, int x, int y) { return (x + TS_G) * P + (y + TS_G); }
+
+// exchange._strip_slices (exchange.py:162-182): (layer, along) -> (x, y)
+void eta_strip_xy(int side, bool sending, int ni, int nj, int along, int layer, int *x, int *y)
+{
+    switch (side) {
+    case TS_WEST: *x = sending ? layer : -2 + layer; *y = along; break;
+    case TS_EAST: *x = sending ? ni - 2 + layer : ni + layer; *y = along; break;
+    case TS_SOUTH: *y = sending ? layer : -2 + layer; *x = along; break;
+    default: *y = sending ? nj - 2 + layer : nj + layer; *x = along; break;
+    }
+}
+
+// exchange._face_strip (exchange.py:185-215): returns (x, y) and the array
+// (1 = m, 2 = n)
+void face_strip_xy(int side, bool sending, bool normal, int ni, int nj, int along, int layer,
+                   int *x, int *y, int *arr)
+{
+    const bool x_side = side <= TS_EAST;
+    const bool low = side == TS_WEST || side == TS_SOUTH;
+    const int n_edge = x_side ? ni : nj;
+    int across;
+    if (normal) across = sending ? (low ? 1 + layer : n_edge - 2 + layer) : (low ? -2 + layer : n_edge + 1 + layer);
+    else        across = sending ? (low ? layer : n_edge - 2 + layer) : (low ? -2 + layer : n_edge + layer);
+    if (x_side) { *x = across; *y = along; *arr = normal ? 1 : 2; }
+    else        { *x = along; *y = across; *arr = normal ? 2 : 1; }
+}
+
+const int kOpp[4] = {TS_EAST, TS_WEST, TS_NORTH, TS_SOUTH};
+
+struct DstKey {
+    int32_t blk, arr, idx;
+    bool operator==(const DstKey &o) const { return blk == o.blk && arr == o.arr && idx == o.idx; }
+};
+struct DstHash {
+    size_t operator()(const DstKey &k) const
+    {
+        return std::hash<long long>()(((long long)k.blk << 34) ^ ((long long)k.arr << 32) ^ (unsigned)k.idx);
+    }
+};
+
+// keep the LAST writer of every destination (the reference applies entries
+// in order, runner.py:178-186), preserving order among survivors
+std::vector<Copy> dedup_last(const std::vector<Copy> &in)
+{
+    std::unordered_map<DstKey, size_t, DstHash> last;
+    last.reserve(in.size() * 2);
+    for (size_t k = 0; k < in.size(); ++k) {
+        const int arr = (in[k].src_blk >> 28) & 3;
+        last[{in[k].dst_blk, arr, in[k].dst_idx}] = k;
+    }
+    std::vector<Copy> out;
+    out.reserve(last.size());
+    for (size_t k = 0; k < in.size(); ++k) {
+        const int arr = (in[k].src_blk >> 28) & 3;
+        if (last[{in[k].dst_blk, arr, in[k].dst_idx}] == k) out.push_back(in[k]);
+    }
+    return out;
+}
+
+template <typename Tv>
+int upload(Tv **dptr, const std::vector<Tv> &v)
+{
+    if (v.empty()) return TS_OK;
+    CK(cudaMalloc((void **)dptr, v.size() * sizeof(Tv)));
+    CK(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(Tv), cudaMemcpyHostToDevice));
+    return TS_OK;
+}
+
+int create_impl(const ts_desc *d, ts_handle *h)
+{
+    if (!d) return fail(TS_ERR_INVALID, "null descriptor");
+    if (d->abi_version != TS_ABI_VERSION)
+        return fail(TS_ERR_INVALID, "ABI version %d, library is %d", d->abi_version, TS_ABI_VERSION);
+    if (d->n_blocks <= 0 || !d->blocks) return fail(TS_ERR_INVALID, "system has no blocks");
+    if (!(d->dt > 0)) return fail(TS_ERR_INVALID, "dt must be positive, got %g", d->dt);
+    h->device = d->device;
+    h->rank = d->rank;
+    h->nranks = d->n_ranks > 0 ? d->n_ranks : 1;
+    h->dt = d->dt;
+    h->g = d->gravity;
+    h->thr = d->wet_threshold;
+    h->nb = d->n_blocks;
+    if (d->tile_rows > 0) h->T = d->tile_rows;
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    for (auto &e : h->ev) CK(cudaEventCreate(&e));
+    CK(cudaEventCreate(&h->t0));
+    CK(cudaEventCreate(&h->t1));
+
+    // ---- arena
+    h->desc.assign(d->blocks, d->blocks + d->n_blocks);
+    h->hb.assign(h->nb, DevBlock{});
+    std::vector<size_t> off(h->nb, 0), sizes;
+    size_t total = 0;
+    for (int b = 0; b < h->nb; ++b) {
+        const ts_block_desc &bd = d->blocks[b];
+        if (bd.ni < 1 || bd.nj < 1) return fail(TS_ERR_INVALID, "block %lld is %dx%d", (long long)bd.block_id, bd.ni, bd.nj);
+        if (bd.owner != h->rank) continue;
+        if (!bd.h_ext || !bd.eta0) return fail(TS_ERR_INVALID, "block %lld: missing h_ext/eta0", (long long)bd.block_id);
+        const size_t P = align_up((size_t)bd.nj + 5, 4);
+        const size_t cell = (size_t)(bd.ni + 4) * P, mrows = (size_t)(bd.ni + 5) * P, acc = (size_t)bd.ni * P;
+        size_t need = 0;
+        need += 2 * align_up(cell * 8, 256) + 2 * align_up(mrows * 8, 256) + 2 * align_up(cell * 8, 256);
+        need += align_up(cell * 8, 256) * (bd.nman_ext ? 2 : 1);
+        need += 3 * align_up(acc * 8, 256);
+        off[b] = total;
+        total += need;
+    }
+    h->arena_bytes = total;
+    if (total) {
+        CK(cudaMalloc((void **)&h->arena, total));
+        CK(cudaMemset(h->arena, 0, total));
+    }
+    for (int b = 0; b < h->nb; ++b) {
+        const ts_block_desc &bd = d->blocks[b];
+        DevBlock &B = h->hb[b];
+        B.ni = bd.ni;
+        B.nj = bd.nj;
+        B.P = (int)align_up((size_t)bd.nj + 5, 4);
+        B.order = b;
+        B.r = d->dt / bd.dx;
+        B.grr = d->gravity * B.r;
+        B.dtg = d->dt * d->gravity;
+        B.kf = (B.dtg * bd.manning) * bd.manning;
+        B.has_nman = bd.nman_ext ? 1 : 0;
+        if (bd.owner != h->rank) continue;
+        const size_t P = B.P;
+        const size_t cell = (size_t)(bd.ni + 4) * P, mrows = (size_t)(bd.ni + 5) * P, acc = (size_t)bd.ni * P;
+        char *p = h->arena + off[b];
+        auto take = [&](size_t n) { double *q = (double *)p; p += align_up(n * 8, 256); return q; };
+        B.eta[0] = take(cell); B.eta[1] = take(cell);
+        B.m[0] = take(mrows); B.m[1] = take(mrows);
+        B.n[0] = take(cell); B.n[1] = take(cell);
+        B.h = take(cell);
+        B.nman = bd.nman_ext ? take(cell) : nullptr;
+        B.acc_eta = take(acc); B.acc_speed = take(acc); B.acc_inund = take(acc);
+        // h_ext / n_ext with ghosts (kernels.py:53-62, exchange.py:281-300)
+        CK(cudaMemcpy2D(B.h, P * 8, bd.h_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
+                        bd.ni + 4, cudaMemcpyHostToDevice));
+        if (B.nman)
+            CK(cudaMemcpy2D(B.nman, P * 8, bd.nman_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
+                            bd.ni + 4, cudaMemcpyHostToDevice));
+        // set_initial_eta: interior of BOTH buffers (kernels.py:97-101)
+        for (int k = 0; k < 2; ++k)
+            CK(cudaMemcpy2D(B.eta[k] + 2 * P + 2, P * 8, bd.eta0, (size_t)bd.nj * 8, (size_t)bd.nj * 8,
+                            bd.ni, cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc((void **)&h->d_blocks, sizeof(DevBlock) * h->nb));
+    CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
+    CK(cudaMalloc((void **)&h->d_err, sizeof(unsigned long long)));
+    CK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
+    CK(cudaMalloc((void **)&h->d_accflag, sizeof(int)));
+    CK(cudaMemset(h->d_accflag, 0, sizeof(int)));
+
+    // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1)
+    for (int k = 0; k < 4; ++k) h->groups[k].W = k + 1;
+    for (int b = 0; b < h->nb; ++b) {
+        if (d->blocks[b].owner != h->rank) continue;
+        const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
+        int W, w;
+        if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
+        else { W = 4; w = 126; }
+        for (int j0 = 0; j0 < nj + 1; j0 += w)
+            for (int i0 = 0; i0 < ni + 1; i0 += h->T)
+                h->groups[W - 1].tiles.push_back(
+                    Tile{b, i0, std::min(i0 + h->T, ni + 1), j0, std::min(j0 + w, nj + 1), 0});
+    }
+    for (auto &gr : h->groups)
+        if (int rc = upload(&gr.d, gr.tiles)) return rc;
+
+    auto owned = [&](int b) { return b >= 0 && b < h->nb && d->blocks[b].owner == h->rank; };
+    auto check_blk = [&](int b) { return b >= 0 && b < h->nb; };
+    size_t stage_len = 0;
+
+    // ---- restriction segments (coupling.py:278-315)
+    {
+        std::vector<RSeg> segs;
+        std::unordered_set<long long> written, read;
+        auto key = [](int b, int x, int y) { return ((long long)b << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8); };
+        int64_t first = 0;
+        for (int k = 0; k < d->n_restrict; ++k) {
+            const ts_eta_segment &s = d->restrict_segs[k];
+            if (!check_blk(s.parent) || !check_blk(s.child) || s.side < 0 || s.side > 3)
+                return fail(TS_ERR_INVALID, "bad restriction segment %d", k);
+            const int count = s.parent_hi - s.parent_lo;
+            if (count < 0 || s.child_hi - s.child_lo != 3 * count)
+                return fail(TS_ERR_INVALID, "restriction segment %d: spans disagree", k);
+            if (!owned(s.child) || count == 0) continue;
+            const bool ns = s.side >= TS_SOUTH;
+            segs.push_back(RSeg{s.child, s.parent, ns, s.child_lo, s.ring_start, s.parent_line,
+                                s.parent_lo, count, first});
+            first += count;
+            for (int p = 0; p < count; ++p) {
+                written.insert(key(s.parent, ns ? s.parent_lo + p : s.parent_line, ns ? s.parent_line : s.parent_lo + p));
+                for (int u = 0; u < 3; ++u)
+                    for (int v = 0; v < 3; ++v) {
+                        const int x = ns ? s.child_lo + 3 * p + u : s.ring_start + u;
+                        const int y = ns ? s.ring_start + v : s.child_lo + 3 * p + v;
+                        read.insert(key(s.child, x, y));
+                    }
+            }
+        }
+        for (long long w : written)
+            if (read.count(w)) { h->r_two_pass = true; break; }
+        h->r_elems = first;
+        h->n_rseg = (int)segs.size();
+        stage_len = std::max(stage_len, (size_t)first);
+        if (int rc = upload(&h->d_rseg, segs)) return rc;
+    }
+    // ---- prolongation segments (coupling.py:318-340)
+    {
+        std::vector<PSeg> segs;
+        std::unordered_set<long long> written, read;
+        auto key = [](int b, int arr, int x, int y) {
+            return ((long long)b << 44) ^ ((long long)arr << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8);
+        };
+        int64_t first = 0;
+        for (int k = 0; k < d->n_prolong; ++k) {
+            const ts_flux_segment &s = d->prolong_segs[k];
+            if (!check_blk(s.parent) || !check_blk(s.child) || s.side < 0 || s.side > 3)
+                return fail(TS_ERR_INVALID, "bad prolongation segment %d", k);
+            const int count = s.parent_hi - s.parent_lo;
+            if (count < 0 || s.child_hi - s.child_lo != 3 * count)
+                return fail(TS_ERR_INVALID, "prolongation segment %d: spans disagree", k);
+            if (!owned(s.parent) || count == 0) continue;
+            const bool ns = s.side >= TS_SOUTH;
+            segs.push_back(PSeg{s.parent, s.child, ns, s.child_lo, s.child_face_line, s.parent_face_line,
+                                s.parent_lo, count, first});
+            first += 3 * count;
+            const int arr = ns ? 2 : 1;
+            for (int p = 0; p < count; ++p) {
+                read.insert(key(s.parent, arr, ns ? s.parent_lo + p : s.parent_face_line,
+                                ns ? s.parent_face_line : s.parent_lo + p));
+                for (int u = 0; u < 3; ++u) {
+                    const int a = s.child_lo + 3 * p + u;
+                    written.insert(key(s.child, arr, ns ? a : s.child_face_line, ns ? s.child_face_line : a));
+                }
+            }
+        }
+        for (long long w : written)
+            if (read.count(w)) { h->p_two_pass = true; break; }
+        h->p_elems = first;
+        h->n_pseg = (int)segs.size();
+        stage_len = std::max(stage_len, (size_t)first);
+        if (int rc = upload(&h->d_pseg, segs)) return rc;
+    }
+    if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
+
+    // ---- halo strips (exchange.py:218-275) as deduplicated element copies
+    {
+        std::vector<Copy> eta, flux;
+        for (int k = 0; k < d->n_halo; ++k) {
+            const ts_halo_entry &e = d->halo[k];
+            if (!check_blk(e.sender) || !check_blk(e.receiver) || e.side < 0 || e.side > 3)
+                return fail(TS_ERR_INVALID, "bad halo entry %d", k);
+            const int span = e.send_hi - e.send_lo;
+            if (span < 0 || e.recv_hi - e.recv_lo != span)
+                return fail(TS_ERR_INVALID, "halo entry %d: spans disagree", k);
+            const ts_block_desc &S = d->blocks[e.sender], &R = d->blocks[e.receiver];
+            const int Ps = h->hb[e.sender].P, Pr = h->hb[e.receiver].P;
+            const int rside = kOpp[e.side];
+            for (int l = 0; l < 2; ++l)
+                for (int a = 0; a < span; ++a) {
+                    int sx, sy, rx, ry;
+                    eta_strip_xy(e.side, true, S.ni, S.nj, e.send_lo + a, l, &sx, &sy);
+                    eta_strip_xy(rside, false, R.ni, R.nj, e.recv_lo + a, l, &rx, &ry);
+                    eta.push_back(Copy{e.sender, e.receiver, pidx(Ps, sx, sy), pidx(Pr, rx, ry)});
+                }
+            for (int normal = 1; normal >= 0; --normal) {
+                const int len = normal ? span : span + 1;
+                for (int l = 0; l < 2; ++l)
+                    for (int a = 0; a < len; ++a) {
+                        int sx, sy, sarr, rx, ry, rarr;
+                        face_strip_xy(e.side, true, normal, S.ni, S.nj, e.send_lo + a, l, &sx, &sy, &sarr);
+                        face_strip_xy(rside, false, normal, R.ni, R.nj, e.recv_lo + a, l, &rx, &ry, &rarr);
+                        flux.push_back(Copy{e.sender | (sarr << 28), e.receiver, pidx(Ps, sx, sy), pidx(Pr, rx, ry)});
+                    }
+            }
+        }
+        eta = dedup_last(eta);
+        flux = dedup_last(flux);
+        std::vector<Copy> eta_own, flux_own;
+        for (auto &c : eta) if (owned(c.src_blk & 0x0fffffff)) eta_own.push_back(c);
+        for (auto &c : flux) if (owned(c.src_blk & 0x0fffffff)) flux_own.push_back(c);
+        h->n_heta = (int64_t)eta_own.size();
+        h->n_hflux = (int64_t)flux_own.size();
+        if (int rc = upload(&h->d_heta, eta_own)) return rc;
+        if (int rc = upload(&h->d_hflux, flux_own)) return rc;
+    }
+    // ---- outer-boundary edges (kernels.py:274-306)
+    {
+        std::vector<Copy> edges;
+        std::unordered_set<long long> dsts;
+        bool serial = false;
+        for (int k = 0; k < d->n_edges; ++k) {
+            const ts_edge &e = d->edges[k];
+            if (!check_blk(e.block) || e.side < 0 || e.side > 3 || (e.kind != TS_REFLECTIVE && e.kind != TS_RADIATION))
+                return fail(TS_ERR_INVALID, "bad edge %d", k);
+            if (!owned(e.block)) continue;
+            const ts_block_desc &B = d->blocks[e.block];
+            const int P = h->hb[e.block].P;
+            const bool xs = e.side <= TS_EAST;
+            const int arr = xs ? 1 : 2;
+            const int n_edge = xs ? B.ni : B.nj;
+            const int edge = (e.side == TS_WEST || e.side == TS_SOUTH) ? 0 : n_edge;
+            const int inner = (e.side == TS_WEST || e.side == TS_SOUTH) ? 1 : n_edge - 1;
+            for (int a = e.lo; a < e.hi; ++a) {
+                const int dst = xs ? pidx(P, edge, a) : pidx(P, a, edge);
+                const int src = e.kind == TS_REFLECTIVE ? -1 : (xs ? pidx(P, inner, a) : pidx(P, a, inner));
+                if (src >= 0 && dsts.count(((long long)e.block << 34) ^ ((long long)arr << 32) ^ (unsigned)src)) serial = true;
+                dsts.insert(((long long)e.block << 34) ^ ((long long)arr << 32) ^ (unsigned)dst);
+                edges.push_back(Copy{e.block | (arr << 28), e.block, src, dst});
+            }
+        }
+        // a radiation source written by an earlier edge, or a repeated
+        // destination, needs the reference's sequential order
+        if (dsts.size() != edges.size()) serial = true;
+        for (auto &c : edges)
+            if (c.src_idx >= 0 && dsts.count(((long long)c.dst_blk << 34) ^ ((long long)((c.src_blk >> 28) & 3) << 32) ^ (unsigned)c.src_idx))
+                serial = true;
+        h->edge_serial = serial;
+        h->n_edge = (int64_t)edges.size();
+        if (int rc = upload(&h->d_edge, edges)) return rc;
+    }
+    CK(cudaDeviceSynchronize());
+    return build_graphs(h);
+}
+
+int check_error(ts_handle *h)
+{
+    unsigned long long key;
+    CK(cudaMemcpy(&key, h->d_err, sizeof key, cudaMemcpyDeviceToHost));
+    if (key == TS_NO_ERROR) return TS_OK;
+    const int order = (int)(key >> 50), what = (int)((key >> 48) & 3);
+    const long long i = (long long)((key >> 24) & 0xffffff) - 4, j = (long long)(key & 0xffffff) - 4;
+    static const char *names[3] = {"water level", "x-flux", "y-flux"};
+    return fail(TS_ERR_NUMERICS, "non-finite %s in block %lld at local cell (%lld, %lld)", names[what],
+                (long long)h->desc[order].block_id, i, j);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ts_last_error(void) { return g_err.c_str(); }
+int ts_abi_version(void) { return TS_ABI_VERSION; }
+
+int ts_create(const ts_desc *desc, ts_handle **out)
+{
+    if (!out) return fail(TS_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    ts_handle *h = new ts_handle();
+    int rc = create_impl(desc, h);
+    if (rc) {
+        std::string keep = g_err;
+        ts_destroy(h);
+        g_err = keep;
+        return rc;
+    }
+    *out = h;
+    return TS_OK;
+}
+
+int ts_run(ts_handle *h, int64_t n_steps)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    if (n_steps < 0) return fail(TS_ERR_INVALID, "negative step count");
+    CK(cudaSetDevice(h->device));
+    if (int rc = check_error(h)) return rc;
+    if (n_steps == 0) return TS_OK;
+    cudaStream_t s = h->stream;
+    int64_t done = 0;
+    // the first step of this call runs eagerly with phase events: its
+    // per-phase times apportion the run's device time to the routines
+    // (runner.ROUTINES); the fold flag is cleared for the very first step
+    // of the simulation (no previous outputs exist yet)
+    if (h->steps == 0) CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
+    CK(cudaEventRecord(h->t0, s));
+    if (int rc = enqueue_step(h, s, h->cur, true, nullptr)) return rc;
+    float ph[7] = {0};
+    CK(cudaEventSynchronize(h->ev[kPhaseEvents - 1]));
+    for (int k = 0; k < 7; ++k) CK(cudaEventElapsedTime(&ph[k], h->ev[k], h->ev[k + 1]));
+    h->cur ^= 1;
+    h->steps += 1;
+    done = 1;
+    CK(cudaMemsetAsync(h->d_accflag, 1, 1, s));
+    const int64_t chunk = 256;
+    double sum_mass = 0, sum_mom = 0, sum_step = 0;
+    int64_t timed = 0;
+    while (done < n_steps) {
+        const int64_t n = std::min(chunk, n_steps - done);
+        if (h->timing && h->pool.size() < (size_t)(5 * n)) {
+            const size_t old = h->pool.size();
+            h->pool.resize(5 * n);
+            for (size_t k = old; k < h->pool.size(); ++k) CK(cudaEventCreate(&h->pool[k]));
+        }
+        for (int64_t k = 0; k < n; ++k) {
+            if (h->timing)
+                for (int q = 0; q < 5; ++q)
+                    CK(cudaGraphExecEventRecordNodeSetEvent(h->gexec[h->cur], h->ev_node[h->cur][kTimed[q]],
+                                                            h->pool[5 * k + q]));
+            CK(cudaGraphLaunch(h->gexec[h->cur], s));
+            h->cur ^= 1;
+        }
+        h->steps += n;
+        done += n;
+        if (h->timing || done < n_steps) {
+            CK(cudaStreamSynchronize(s));
+            if (int rc = check_error(h)) return rc;
+        }
+        if (h->timing) {
+            for (int64_t k = 0; k < n; ++k) {
+                float a = 0, b = 0, c = 0;
+                CK(cudaEventElapsedTime(&a, h->pool[5 * k + 0], h->pool[5 * k + 1]));
+                CK(cudaEventElapsedTime(&b, h->pool[5 * k + 2], h->pool[5 * k + 3]));
+                CK(cudaEventElapsedTime(&c, h->pool[5 * k + 0], h->pool[5 * k + 4]));
+                sum_mass += a; sum_mom += b; sum_step += c;
+            }
+            timed += n;
+            // restore the graphs' own phase events
+            for (int c = 0; c < 2; ++c)
+                for (int q = 0; q < 5; ++q)
+                    CK(cudaGraphExecEventRecordNodeSetEvent(h->gexec[c], h->ev_node[c][kTimed[q]], h->ev[kTimed[q]]));
+        }
+    }
+    if (timed) {
+        h->mass_s = sum_mass / timed / 1e3;
+        h->mom_s = sum_mom / timed / 1e3;
+        h->step_s = sum_step / timed / 1e3;
+    }
+    if (int rc = enqueue_flush(h, s, h->cur)) return rc;
+    CK(cudaEventRecord(h->t1, s));
+    CK(cudaStreamSynchronize(s));
+    float tot = 0;
+    CK(cudaEventElapsedTime(&tot, h->t0, h->t1));
+    const double sum = ph[0] + ph[1] + ph[2] + ph[3] + ph[4] + ph[5] + ph[6];
+    const double scale = sum > 0 ? (tot / 1e3) / sum : 0.0;
+    // ROUTINES order: mass, momentum, restrict, prolong, halo-eta, halo-flux,
+    // output.  momentum includes the edge rules like Simulation._momentum
+    // (runner.py:111-117); output is fused into mass.
+    h->routines[0] = ph[0] * scale;
+    h->routines[1] = (ph[3] + ph[4]) * scale;
+    h->routines[2] = ph[1] * scale;
+    h->routines[3] = ph[5] * scale;
+    h->routines[4] = ph[2] * scale;
+    h->routines[5] = ph[6] * scale;
+    h->routines[6] = 0.0;
+    h->total = tot / 1e3;
+    return check_error(h);
+}
+
+int ts_set_timing(ts_handle *h, int32_t on)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    h->timing = on != 0;
+    return TS_OK;
+}
+
+int ts_phase(ts_handle *h, int32_t phase)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    CK(cudaSetDevice(h->device));
+    cudaStream_t s = h->stream;
+    const StepArgs a = args_of(h, h->cur);
+    switch (phase) {
+    case TS_PH_MASS:
+        for (auto &gr : h->groups)
+            if (!gr.tiles.empty()) launch_mass(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
+        break;
+    case TS_PH_RESTRICT:
+        if (h->r_two_pass) {
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 2, s);
+        } else {
+            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, nullptr, 0, s);
+        }
+        break;
+    case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
+    case TS_PH_MOMENTUM:
+        for (auto &gr : h->groups)
+            if (!gr.tiles.empty()) launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s);
+        break;
+    case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
+    case TS_PH_PROLONG:
+        if (h->p_two_pass) {
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 1, s);
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 2, s);
+        } else {
+            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, nullptr, 0, s);
+        }
+        break;
+    case TS_PH_HALO_FLUX: launch_copies(a, h->d_hflux, h->n_hflux, false, s); break;
+    case TS_PH_OUTPUT:
+        if (int rc = enqueue_flush(h, s, h->cur ^ 1)) return rc;
+        break;
+    case TS_PH_SWAP: h->cur ^= 1; return TS_OK;
+    default: return fail(TS_ERR_INVALID, "unknown phase %d", phase);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(s));
+    return check_error(h);
+}
+
+int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_t len)
+{
+    if (!h || !out) return fail(TS_ERR_INVALID, "null argument");
+    FieldGeom g;
+    if (int rc = field_geom(h, block, field, &g)) return rc;
+    if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy2D(out, (size_t)g.cols * 8, g.ptr, (size_t)g.pitch * 8, (size_t)g.cols * 8, g.rows,
+                    cudaMemcpyDeviceToHost));
+    return TS_OK;
+}
+
+int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, int64_t len)
+{
+    if (!h || !in) return fail(TS_ERR_INVALID, "null argument");
+    FieldGeom g;
+    if (int rc = field_geom(h, block, field, &g)) return rc;
+    if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy2D(g.ptr, (size_t)g.pitch * 8, in, (size_t)g.cols * 8, (size_t)g.cols * 8, g.rows,
+                    cudaMemcpyHostToDevice));
+    return TS_OK;
+}
+
+int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    unsigned long long key;
+    CK(cudaSetDevice(h->device));
+    CK(cudaMemcpy(&key, h->d_err, sizeof key, cudaMemcpyDeviceToHost));
+    if (key == TS_NO_ERROR) {
+        if (block) *block = -1;
+        return TS_OK;
+    }
+    if (block) *block = (int32_t)(key >> 50);
+    if (what) *what = (int32_t)((key >> 48) & 3);
+    if (i) *i = (int64_t)((key >> 24) & 0xffffff) - 4;
+    if (j) *j = (int64_t)(key & 0xffffff) - 4;
+    return TS_OK;
+}
+
+int ts_timings(ts_handle *h, double *routines7, double *total)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    if (routines7) std::memcpy(routines7, h->routines, sizeof h->routines);
+    if (total) *total = h->total;
+    return TS_OK;
+}
+
+int64_t ts_steps_done(ts_handle *h) { return h ? h->steps : -1; }
+int64_t ts_device_bytes(ts_handle *h) { return h ? (int64_t)h->arena_bytes : -1; }
+int32_t ts_launches_per_step(ts_handle *h) { return h ? h->launches : -1; }
+
+int ts_kernel_seconds(ts_handle *h, double *mass_s, double *momentum_s, double *step_s)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    if (mass_s) *mass_s = h->mass_s;
+    if (momentum_s) *momentum_s = h->mom_s;
+    if (step_s) *step_s = h->step_s;
+    return TS_OK;
+}
+
+int ts_stream(ts_handle *h, void **stream)
+{
+    if (!h || !stream) return fail(TS_ERR_INVALID, "null argument");
+    *stream = (void *)h->stream;
+    return TS_OK;
+}
+
+void ts_destroy(ts_handle *h)
+{
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto &g : h->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : h->graph)
+        if (g) cudaGraphDestroy(g);
+    for (auto &gr : h->groups) cudaFree(gr.d);
+    cudaFree(h->d_rseg);
+    cudaFree(h->d_pseg);
+    cudaFree(h->d_heta);
+    cudaFree(h->d_hflux);
+    cudaFree(h->d_edge);
+    cudaFree(h->d_stage);
+    cudaFree(h->d_err);
+    cudaFree(h->d_accflag);
+    cudaFree(h->d_blocks);
+    cudaFree(h->arena);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : h->pool) cudaEventDestroy(e);
+    if (h->t0) cudaEventDestroy(h->t0);
+    if (h->t1) cudaEventDestroy(h->t1);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+int ts_ipc_export(ts_handle *h, void *out, int64_t len)
+{
+    (void)h; (void)out; (void)len;
+    return fail(TS_ERR_INVALID, "multi-GPU exchange not built into this library version");
+}
+
+int ts_ipc_import(ts_handle *h, int32_t peer_rank, const void *in, int64_t len)
+{
+    (void)h; (void)peer_rank; (void)in; (void)len;
+    return fail(TS_ERR_INVALID, "multi-GPU exchange not built into this library version");
+}
+
+void ts_cbrt_host(const double *in, double *out, int64_t n)
+{
+    for (int64_t k = 0; k < n; ++k) out[k] = ts_cbrt(in[k]);
+}
+
+int ts_cbrt_device(int32_t device, const double *in, double *out, int64_t n)
+{
+    if (n <= 0) return TS_OK;
+    CK(cudaSetDevice(device));
+    double *d = nullptr;
+    CK(cudaMalloc((void **)&d, 2 * n * sizeof(double)));
+    CK(cudaMemcpy(d, in, n * sizeof(double), cudaMemcpyHostToDevice));
+    launch_cbrt(d, d + n, n, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, d + n, n * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    return TS_OK;
+}
+
+}  // extern "C"

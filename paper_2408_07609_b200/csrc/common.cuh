@@ -1,0 +1,92 @@
+// Shared device-side types for the nested-grid step.
+//
+// HBM layout: one arena per GPU; every owned block keeps the
+// reference's ghosted BlockState arrays (kernels.py:39-62; halo g = 2) but
+// with a common row pitch P = round_up(nj + 5, 4) doubles, so every row of
+// every array starts 32-byte aligned and a tile of consecutive rows is one
+// contiguous span.  Element (x, y) of an eta/h/nman array (cells x,y in
+// [-2, n+2)) sits at (x+2)*P + (y+2); M face (fx, cy) at (fx+2)*P + cy+2;
+// N (cx, fy) at (cx+2)*P + fy+2; accumulators (i, j) at i*P + j.
+#pragma once
+#include <stdint.h>
+
+#define TS_G 2
+
+struct DevBlock {
+    double *eta[2], *m[2], *n[2];
+    double *h, *nman;
+    double *acc_eta, *acc_speed, *acc_inund;
+    int32_t ni, nj, P, order;       // order = global block index
+    double r;                       // dt / dx                      (kernels.py:134, 242)
+    double grr;                     // grav * r                     (kernels.py:243)
+    double kf;                      // ((dt*grav)*n)*n, scalar n    (kernels.py:240)
+    double dtg;                     // dt * grav
+    int32_t has_nman, pad;
+};
+
+// one unit of the march kernels: rows [i0, i1) x output columns [j0, j1)
+struct Tile {
+    int32_t blk, i0, i1, j0, j1, pad;
+};
+
+// one restriction segment (coupling.EtaSegment + its link)
+struct RSeg {
+    int32_t child, parent, ns, a, ring, pline, pa, count;
+    int64_t first;                  // first element (parent cell) index
+};
+
+// one prolongation segment (coupling.FluxSegment + its link)
+struct PSeg {
+    int32_t parent, child, ns, a, cline, pline, pa, count;
+    int64_t first;                  // first element (child face) index
+};
+
+// element copy: dst[dst_idx] = src[src_idx]; arr 0 eta, 1 m, 2 n (the
+// "new" buffer of each); src_idx < 0 means "write 0" (reflective edge)
+struct Copy {
+    int32_t src_blk, dst_blk, src_idx, dst_idx;   // src_blk holds arr in bits 28..29
+};
+
+#define TS_NO_ERROR 0xffffffffffffffffULL
+
+// first-error key: lexicographic (block order, what, i, j) so atomicMin
+// reports the reference's first raising check (kernels.py:115-120;
+// runner.py serial order); i, j biased by 4 (ghost indices are >= -2)
+__host__ __device__ inline unsigned long long ts_err_key(int order, int what, long long i, long long j)
+{
+    return ((unsigned long long)order << 50) | ((unsigned long long)what << 48)
+         | ((unsigned long long)(i + 4) << 24) | (unsigned long long)(j + 4);
+}
+
+// numpy scalar maximum (NaN propagating, first operand wins ties):
+// (a >= b || isnan(a)) ? a : b
+__host__ __device__ __forceinline__ double np_max(double a, double b)
+{
+    return (a >= b || a != a) ? a : b;
+}
+
+// np.sign: +1, -1, 0 for +-0, NaN for NaN
+__host__ __device__ __forceinline__ double np_sign(double x)
+{
+    return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
+}
+
+// ---- launchers (kernels.cu) ----
+struct StepArgs {
+    const DevBlock *blocks;
+    int cur;                        // "old" buffer index
+    double thr;
+    unsigned long long *err;
+    const int *acc_flag;            // fold previous step's outputs in K_mass
+};
+
+void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool accumulate,
+                 cudaStream_t s);
+void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
+void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
+void launch_restrict(const StepArgs &a, const RSeg *segs, int nseg, int64_t nelem, double *stage,
+                     int mode, cudaStream_t s);
+void launch_prolong(const StepArgs &a, const PSeg *segs, int nseg, int64_t nelem, double *stage,
+                    int mode, cudaStream_t s);
+void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
+void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);

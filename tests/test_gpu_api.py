@@ -1,0 +1,152 @@
+"""The reference's run-level contract on the GPU path (tests/test_runner.py,
+tests/test_acceptance.py of the reference, ported to the product API)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import systems
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(P, system, nr):
+    return P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], nr)
+
+
+def _nan_system(T):
+    return T.NestedGridSystem(levels=[T.GridLevel(1, 10.0, [
+        systems.flat_block(T, 1, (0.0, 0.0), 8, 8, 30.0),
+        T.Block(2, (80.0, 0.0), 8, 8, np.where(np.eye(8, dtype=bool), np.nan, 30.0))])])
+
+
+def test_numerics_error_message_matches_reference(cuda_device, product):
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        want = json.load(f)["nan_bathymetry"]
+    system = _nan_system(product)
+    sim = product.Simulation(system, product.SimulationConfig(dt=0.2), _plan(product, system, 1))
+    with pytest.raises(product.NumericsError) as ei:
+        sim.run(3, threaded=False)
+    assert str(ei.value) == want
+
+
+def test_worker_failure_aborts_threaded_run(cuda_device, product):
+    """tests/test_runner.py:102-112: multi-rank runs wrap it in SimulationAborted."""
+    system = _nan_system(product)
+    sim = product.Simulation(system, product.SimulationConfig(dt=0.2), _plan(product, system, 2))
+    with pytest.raises(product.SimulationAborted):
+        sim.run(3, threaded=True, timeout=5.0)
+
+
+def test_lake_at_rest_bitwise(cuda_device, product):
+    """tests/test_acceptance.py:60-81 (trench, land, island, sub-threshold film)."""
+    n = 150
+    h = np.full((n, n), 30.0)
+    h[:, :20] = 95.0
+    h[120:, :] = -5.0
+    h[40:55, 60:75] = -2.0
+    h[60:80, 80:100] = 0.5e-5
+    T = product
+    system = T.NestedGridSystem(levels=[T.GridLevel(1, 10.0, [T.Block(1, (0.0, 0.0), n, n, h)])])
+    sim = T.Simulation(system, T.SimulationConfig(dt=0.2), _plan(T, system, 1))
+    sim.run(1000, threaded=False)
+    st = sim.states[1]
+    assert np.max(np.abs(st.interior(st.eta_old))) == 0.0
+    assert np.all(st.m_old == 0.0) and np.all(st.n_old == 0.0)
+
+
+def test_mass_conservation_closed_basin(cuda_device, product):
+    """tests/test_acceptance.py:84-102."""
+    n, dx = 120, 10.0
+    T = product
+    system = T.NestedGridSystem(levels=[T.GridLevel(1, dx, [systems.flat_block(T, 1, (0.0, 0.0), n, n, 50.0)])])
+    sim = T.Simulation(system, systems.hump(T, 1.0, 80.0, (600.0, 600.0)), _plan(T, system, 1))
+    st = sim.states[1]
+    vol0 = float(np.sum(st.interior(st.eta_old))) * dx * dx
+    water0 = float(np.sum(50.0 + st.interior(st.eta_old))) * dx * dx
+    sim.run(1000, threaded=False)
+    vol1 = float(np.sum(st.interior(st.eta_old))) * dx * dx
+    assert abs(vol1 - vol0) / water0 < 1e-10
+
+
+def test_mirror_symmetry_with_on_step(cuda_device, product):
+    """tests/test_acceptance.py:105-131 through the serial on_step hook."""
+    n, dx = 60, 10.0
+    h = np.empty((n, n))
+    h[:] = 30.0 - 0.3 * (np.arange(n) + 0.5)[None, :]
+    h[28:32, 10:14] = -2.0
+    T = product
+    system = T.NestedGridSystem(levels=[T.GridLevel(1, dx, [T.Block(1, (0.0, 0.0), n, n, h)])])
+    sim = T.Simulation(system, systems.hump(T, 0.8, 80.0, (300.0, 200.0)), _plan(T, system, 1))
+    worst = [0.0]
+
+    def check(s, step):
+        st = s.states[1]
+        g = st.halo
+        e = st.interior(st.eta_old)
+        a = float(np.max(np.abs(e - e[::-1, :])))
+        m = st.m_old[g:g + n + 1, g:g + n]
+        a = max(a, float(np.max(np.abs(m + m[::-1, :]))))
+        nn = st.n_old[g:g + n, g:g + n + 1]
+        a = max(a, float(np.max(np.abs(nn - nn[::-1, :]))))
+        worst[0] = max(worst[0], a)
+
+    sim.run(500, threaded=False, on_step=check)
+    assert worst[0] < 1e-12
+    with pytest.raises(ValueError):
+        sim.run(1, threaded=True, on_step=check)
+
+
+def test_nested_matches_uniform_fine(cuda_device, product):
+    """tests/test_acceptance.py:265-290."""
+    T = product
+    settings = systems.hump(T, 0.2, 60.0, (240.0, 360.0), dt=0.1)
+    fine = T.NestedGridSystem(levels=[T.GridLevel(1, 3.0, [systems.flat_block(T, 1, (0.0, 0.0), 240, 240, 5.0)])])
+    nested = T.NestedGridSystem(levels=[
+        T.GridLevel(1, 9.0, [systems.flat_block(T, 1, (0.0, 0.0), 80, 80, 5.0)]),
+        T.GridLevel(2, 3.0, [systems.flat_block(T, 2, (180.0, 180.0), 120, 120, 5.0)])])
+    sf = T.Simulation(fine, settings, _plan(T, fine, 1))
+    sn = T.Simulation(nested, settings, _plan(T, nested, 1))
+    worst = 0.0
+    for _ in range(200):
+        sf.run(1, threaded=False)
+        sn.run(1, threaded=False)
+        ef = sf.states[1].interior(sf.states[1].eta_old)[60:180, 60:180]
+        en = sn.states[2].interior(sn.states[2].eta_old)
+        worst = max(worst, float(np.sqrt(np.mean((ef - en) ** 2))))
+    assert worst / 0.2 <= 0.05
+
+
+def test_zero_steps_and_report(cuda_device, product):
+    system, settings, _ = systems.chain(product)
+    sim = product.Simulation(system, settings, _plan(product, system, 2))
+    rep = sim.run(0, threaded=False)
+    assert rep.steps == 0
+    for acc in sim.accumulators.values():
+        assert np.all(acc.max_eta == 0.0) and np.all(acc.max_speed == 0.0)
+    rep = sim.run(5, threaded=True, record_phases=True)
+    assert rep.n_ranks == 2
+    for rt in rep.ranks:
+        assert set(rt.routines) == set(product.ROUTINES)
+        assert all(v >= 0.0 for v in rt.routines.values())
+        assert rt.total >= sum(rt.routines.values()) * 0.5
+    for ctx in sim.contexts:
+        assert ctx.phase_log == list(product.PHASE_SEQUENCE) * 5
+    # seam propagation (tests/test_runner.py:92-98)
+    sim.run(55, threaded=True)
+    assert sim.accumulators[3].max_eta.max() > 1e-4
+
+
+def test_message_trace(cuda_device, product, tmp_path):
+    from paper_2408_07609_b200.runner import read_trace
+    system, settings, _ = systems.kochi(product)
+    sim = product.Simulation(system, settings, _plan(product, system, 4))
+    path = str(tmp_path / "trace.bin")
+    sim.run(3, trace_path=path)
+    recs = read_trace(path)
+    assert recs and all(r[2] != r[3] for r in recs)
+    assert sorted({r[0] for r in recs}) == [0, 1, 2]
+    assert {r[1] for r in recs} <= {0, 1, 2, 3}

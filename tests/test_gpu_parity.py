@@ -1,0 +1,146 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+The gate is bitwise equality (==, NaN-aware) of every array the reference
+exposes — eta/M/N in both buffer roles including ghost rings, the derived
+wet mask against the oracle's stored one, and the three running maxima —
+after full runs of every fixture system, at 1 and 2 ranks, split across
+several ``run`` calls (re-entrancy), on BASELINE configs 1 and 2 at their
+full step counts, on the Kochi-shaped 5-level domain at scale 0.001 and a
+short window at the full 47 M-cell scale.  Phase-level and kernel-level
+parity pin each kernel separately.
+"""
+
+import numpy as np
+import pytest
+
+import systems
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("eta_old", "eta_new", "m_old", "m_new", "n_old", "n_new")
+ACCS = ("max_eta", "max_speed", "max_inundation")
+
+
+def _plan(P, system, nr):
+    return P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], nr)
+
+
+def assert_same(gpu, orc, where=""):
+    for bid, o in orc.states.items():
+        g = gpu.states[bid]
+        for f in FIELDS:
+            a, b = getattr(g, f), getattr(o, f)
+            if not np.array_equal(a, b, equal_nan=True):
+                bad = np.argwhere(~((a == b) | (np.isnan(a) & np.isnan(b))))
+                raise AssertionError(f"{where} block {bid} {f}: {len(bad)} cells differ, first "
+                                     f"{bad[0].tolist()} gpu={a[tuple(bad[0])]!r} "
+                                     f"oracle={b[tuple(bad[0])]!r}")
+        assert np.array_equal(g.wet, o.wet.astype(bool)), (where, bid, "wet")
+        acc = gpu.accumulators[bid]
+        for f in ACCS:
+            assert np.array_equal(getattr(acc, f), getattr(o, f), equal_nan=True), (where, bid, f)
+
+
+@pytest.mark.parametrize("name", systems.SMALL + ("kochi",))
+@pytest.mark.parametrize("nr", (1, 2))
+def test_run_parity(cuda_device, oracle_mod, product, name, nr):
+    system, settings, n = systems.make(product, name)
+    if nr > system.n_blocks:
+        pytest.skip("single block")
+    plan = _plan(product, system, nr)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    assert_same(gpu, orc, "initial")
+    done = 0
+    for chunk in (1, 2, n // 3, n - 3 - n // 3):
+        gpu.run(chunk, threaded=False)
+        orc.run(chunk)
+        done += chunk
+        assert_same(gpu, orc, f"after {done} steps")
+    gpu.close()
+
+
+@pytest.mark.parametrize("name", ("cfg1", "cfg2"))
+def test_baseline_config_parity(cuda_device, oracle_mod, product, name):
+    """BASELINE configs 1 and 2 at their full step counts (1000 / 2000)."""
+    system, settings, n = systems.make(product, name)
+    gpu = product.Simulation(system, settings)
+    orc = oracle_mod.OracleSimulation(system, settings)
+    gpu.run(n, threaded=False)
+    orc.run(n)
+    assert_same(gpu, orc, name)
+    land = sum(int(np.count_nonzero(gpu.accumulators[b].max_inundation)) for b in gpu.states)
+    assert land > 0                       # the wet/dry front moved inland
+
+
+def test_kochi_full_scale_window(cuda_device, oracle_mod, product):
+    """The 47,211,444-cell 5-level domain (BASELINE config 3): a short
+    window, bitwise, with the 4-rank plan's apply order."""
+    system, settings, _ = systems.kochi(product, 1.0)
+    plan = _plan(product, system, 4)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    for chunk in (1, 2):
+        gpu.run(chunk, threaded=False)
+        orc.run(chunk)
+    assert_same(gpu, orc, "kochi-1.0")
+
+
+GPU_PHASES = {"momentum": ("momentum", "edges")}
+
+
+@pytest.mark.parametrize("name", ("identity3", "quad_wetdry"))
+def test_phase_parity(cuda_device, oracle_mod, product, name):
+    """Each phase of runner.PHASE_SEQUENCE separately (gather-then-scatter
+    hazards in identity3; ragged halos and fronts in quad_wetdry)."""
+    system, settings, _ = systems.make(product, name)
+    gpu = product.Simulation(system, settings)
+    orc = oracle_mod.OracleSimulation(system, settings)
+    for step in range(6):
+        for ph in ("mass", "restrict", "halo-eta", "momentum", "prolong", "halo-flux", "output", "swap"):
+            orc.phase(ph)
+            for gph in GPU_PHASES.get(ph, (ph,)):
+                gpu.phase(gph)
+            assert_same(gpu, orc, f"step {step} {ph}")
+
+
+@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("per_cell", (False, True))
+def test_kernel_parity_random_states(cuda_device, oracle_mod, product, seed, per_cell):
+    """update_mass / update_momentum / accumulate on randomised states with
+    land, sub-threshold films, fronts and random ghost fluxes
+    (cf. tests/test_kernels.py:395-419)."""
+    rng = np.random.default_rng(100 + seed)
+    ni, nj = int(rng.integers(5, 70)), int(rng.integers(3, 140))
+    h = rng.uniform(-1.0, 6.0, (ni, nj))
+    h[rng.random((ni, nj)) < 0.15] = 2e-6
+    nman = 0.01 + 0.05 * rng.random((ni, nj)) if per_cell else 0.03
+    blk = product.Block(1, (0.0, 0.0), ni, nj, h, nman)
+    eta0 = np.where(h > 0, rng.normal(0.0, 0.3, (ni, nj)), 0.0)
+    settings = product.SimulationConfig(dt=0.2)
+    system = product.NestedGridSystem(levels=[product.GridLevel(1, 10.0, [blk])])
+    gpu = product.Simulation(system, settings)
+    orc = oracle_mod.single_block_sim(blk, 10.0, settings)
+    m0 = rng.normal(0.0, 0.4, (ni + 5, nj + 4))
+    n0 = rng.normal(0.0, 0.4, (ni + 4, nj + 5))
+    for sim in (gpu, orc):
+        st = sim.states[1]
+        st.eta_old[2:-2, 2:-2] = eta0
+        st.eta_new[2:-2, 2:-2] = eta0
+        st.m_old[...] = m0
+        st.n_old[...] = n0
+    orc.states[1].refresh_wet(settings.wet_threshold)
+    for ph in ("mass", "momentum", "output", "output"):
+        orc.phase(ph)
+        gpu.phase(ph)
+        assert_same(gpu, orc, ph)
+
+
+def test_device_cbrt_bitwise(cuda_device, oracle_mod):
+    from paper_2408_07609_b200 import _native
+    rng = np.random.default_rng(5)
+    x = np.concatenate([np.exp(rng.uniform(np.log(1e-8), np.log(1e6), 2_000_000)),
+                        2.0 ** np.arange(-60, 60.0), [0.0, -0.0, np.inf, -8.0, 5e-324, 1e-310]])
+    d = _native.cbrt_device(x)
+    assert np.array_equal(d.view(np.uint64), _native.cbrt_host(x).view(np.uint64))
+    assert np.array_equal(d.view(np.uint64), oracle_mod.cbrt(x).view(np.uint64))
