@@ -115,9 +115,14 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
 {
     const StepArgs a = args_of(h, cur);
     int n = 0;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(s, &cap));
     auto mark = [&](int k) -> int {
         if (!events) return 0;
-        CK(cudaEventRecordWithFlags(h->ev[k], s, cudaEventRecordExternal));
+        if (cap == cudaStreamCaptureStatusActive)
+            CK(cudaEventRecordWithFlags(h->ev[k], s, cudaEventRecordExternal));
+        else
+            CK(cudaEventRecord(h->ev[k], s));
         return 0;
     };
     if (mark(0)) return TS_ERR_CUDA;

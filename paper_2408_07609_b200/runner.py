@@ -179,9 +179,12 @@ class DeviceBlockState:
 
     @property
     def wet(self):
-        """Derived wet flags of the new buffer, h_ext + eta_new >= thr (what the
-        reference stores, kernels.py:103-105)."""
-        return (self.h_ext + self.eta_new) >= self._thr
+        """The reference's stored wet flags, derived: h_ext + eta >= thr for
+        the buffer its last writer used (kernels.py:103-105, 155; exchange.py
+        :255-257; coupling.py:315) — eta_new within a step, eta_old after the
+        step's swap."""
+        eta = self.eta_old if self._sim._wet_role == "old" else self.eta_new
+        return (self.h_ext + eta) >= self._thr
 
     def interior(self, arr):
         g = self.halo
@@ -261,6 +264,7 @@ class Simulation:
         self.accumulators = {b.block_id: DeviceAccumulators(self, self.index[b.block_id], b)
                              for _, b in ordered}
         self.steps_done = 0
+        self._wet_role = "new"
 
     # -- C ABI descriptor -------------------------------------------------
     def _create(self, ordered, tile_rows):
@@ -345,6 +349,8 @@ class Simulation:
     def _device_run(self, n, threaded):
         rc = N.lib().ts_run(self._h, n)
         self._invalidate()
+        if n:
+            self._wet_role = "old"
         if rc == N.TS_ERR_NUMERICS:
             self._raise_numerics(threaded)
         N.check(rc)
@@ -420,6 +426,7 @@ class Simulation:
         self._sync_in()
         rc = N.lib().ts_phase(self._h, N.PHASES[name])
         self._invalidate()
+        self._wet_role = "old" if name == "swap" else "new"
         if rc == N.TS_ERR_NUMERICS:
             self._raise_numerics(False)
         N.check(rc)
