@@ -24,6 +24,7 @@
 
 #include "cbrt.cuh"
 #include "common.cuh"
+#include "fastmath.cuh"
 
 namespace {
 
@@ -41,8 +42,52 @@ __device__ __forceinline__ void report(unsigned long long *err, int order, int w
 }
 
 // ------------------------------------------------------------------ mass
-// One thread per interior column j, marching down rows [i0, i1) of a tile;
-// M face i of row i+1 is carried in a register.
+// accumulate_outputs for one cell (kernels.py:327-343); returns false if a
+// batched fast op was out of range (caller redoes it with fold_cell_ieee)
+__device__ __forceinline__ bool fold_cell(const DevBlock *B, size_t ac, double e, double h, double d,
+                                          double Ml, double Mr, double Nl, double Nr, double thr)
+{
+    const bool w = d >= thr;
+    const double mc = 0.5 * (Ml + Mr);
+    const double nc = 0.5 * (Nl + Nr);
+    const double ds = np_max(d, thr);
+    bool ok = true;
+    const double y = ts_rcp(ds);
+    const double u = ts_div(mc, ds, y, ok), v = ts_div(nc, ds, y, ok);
+    const double sp = ts_sqrt(u * u + v * v, ok);
+    if (!ok) return false;
+    if (w) {
+        const double me = B->acc_eta[ac], nme = np_max(me, e);
+        if (!(nme == me || (nme != nme && me != me))) B->acc_eta[ac] = nme;
+        const double ms = B->acc_speed[ac], nms = np_max(ms, sp);
+        if (!(nms == ms || (nms != nms && ms != ms))) B->acc_speed[ac] = nms;
+        if (h < 0.0) {
+            const double mi = B->acc_inund[ac], nmi = np_max(mi, d);
+            if (!(nmi == mi || (nmi != nmi && mi != mi))) B->acc_inund[ac] = nmi;
+        }
+    }
+    return true;
+}
+
+__device__ __noinline__ void fold_cell_ieee(const DevBlock *B, size_t ac, double e, double h, double d,
+                                            double Ml, double Mr, double Nl, double Nr, double thr)
+{
+    const bool w = d >= thr;
+    const double mc = 0.5 * (Ml + Mr);
+    const double nc = 0.5 * (Nl + Nr);
+    const double ds = np_max(d, thr);
+    const double u = mc / ds, v = nc / ds;
+    const double sp = sqrt(u * u + v * v);
+    if (w) {
+        B->acc_eta[ac] = np_max(B->acc_eta[ac], e);
+        B->acc_speed[ac] = np_max(B->acc_speed[ac], sp);
+        if (h < 0.0) B->acc_inund[ac] = np_max(B->acc_inund[ac], d);
+    }
+}
+
+// One thread per interior column j, marching down rows [i0, i1) of a tile,
+// unrolled so several rows' loads are in flight; M face i of row i+1 is
+// carried in a register.
 template <int W, int TPC, bool FOLD>
 __global__ void __launch_bounds__(32 * W * TPC)
 k_mass(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
@@ -68,6 +113,7 @@ k_mass(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
     const bool fold = FOLD && (*a.acc_flag != 0);
     size_t row = (size_t)(tl.i0 + TS_G) * P + j + TS_G;
     double Mi = __ldg(mo + row);
+#pragma unroll 4
     for (int i = tl.i0; i < iend; ++i, row += P) {
         const double Mi1 = __ldg(mo + row + P);
         const double Nj = __ldg(no + row), Nj1 = __ldg(no + row + 1);
@@ -77,33 +123,13 @@ k_mass(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
             // accumulate_outputs of the previous step (kernels.py:322-343):
             // its eta_new/m_new/n_new are this step's old buffers
             const size_t ac = (size_t)i * P + j;
-            const bool w = d >= thr;
-            if (w) {
-                const double me = B->acc_eta[ac];
-                const double nme = np_max(me, e0);
-                if (!(nme == me || (nme != nme && me != me))) B->acc_eta[ac] = nme;
-            }
-            const double mc = 0.5 * (Mi + Mi1);
-            const double nc = 0.5 * (Nj + Nj1);
-            const double ds = np_max(d, thr);
-            const double u = mc / ds, v = nc / ds;
-            const double sp = sqrt(u * u + v * v);
-            if (w) {
-                const double ms = B->acc_speed[ac];
-                const double nms = np_max(ms, sp);
-                if (!(nms == ms || (nms != nms && ms != ms))) B->acc_speed[ac] = nms;
-                if (h < 0.0) {
-                    const double mi = B->acc_inund[ac];
-                    const double nmi = np_max(mi, d);
-                    if (!(nmi == mi || (nmi != nmi && mi != mi))) B->acc_inund[ac] = nmi;
-                }
-            }
+            if (!fold_cell(B, ac, e0, h, d, Mi, Mi1, Nj, Nj1, thr))
+                fold_cell_ieee(B, ac, e0, h, d, Mi, Mi1, Nj, Nj1, thr);
         }
-        // update_mass (kernels.py:134-155)
+        // update_mass (kernels.py:134-155); wet_old derived as h + eta_old >= thr
         const double div = r * (Mi1 - Mi) + r * (Nj1 - Nj);
         double e = e0 - div;
-        const bool wet_old = d >= thr;
-        if (!wet_old && div != 0.0) e = np_max(e0, -h) - div;
+        if (!(d >= thr) && div != 0.0) e = np_max(e0, -h) - div;
         if (div != 0.0 && h + e < 0.0) e = -h;
         if (!isfinite(e)) report(a.err, B->order, 0, i, j);
         en[row] = e;
@@ -128,38 +154,34 @@ k_accum(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
     const int iend = min(tl.i1, ni);
     const double *eta = B->eta[a.cur], *m = B->m[a.cur], *n = B->n[a.cur];
     const double thr = a.thr;
+#pragma unroll 4
     for (int i = tl.i0; i < iend; ++i) {
         const size_t row = (size_t)(i + TS_G) * P + j + TS_G, ac = (size_t)i * P + j;
         const double e = eta[row], h = B->h[row], d = h + e;
-        const bool w = d >= thr;
-        if (w) B->acc_eta[ac] = np_max(B->acc_eta[ac], e);
-        const double mc = 0.5 * (m[row] + m[row + P]);
-        const double nc = 0.5 * (n[row] + n[row + 1]);
-        const double ds = np_max(d, thr);
-        const double u = mc / ds, v = nc / ds;
-        const double sp = sqrt(u * u + v * v);
-        if (w) B->acc_speed[ac] = np_max(B->acc_speed[ac], sp);
-        if (w && h < 0.0) B->acc_inund[ac] = np_max(B->acc_inund[ac], d);
+        const double Ml = m[row], Mr = m[row + P], Nl = n[row], Nr = n[row + 1];
+        if (!fold_cell(B, ac, e, h, d, Ml, Mr, Nl, Nr, thr))
+            fold_cell_ieee(B, ac, e, h, d, Ml, Mr, Nl, Nr, thr);
     }
 }
 
 // -------------------------------------------------------------- momentum
-// Face prelims of _momentum_axis (kernels.py:173-215) for one face.
+// Face quantities of _momentum_axis (kernels.py:173-215) for one face with
+// left/right cells (el, hl, Dl = hl + el) | (er, hr, Dr).
 struct Face {
     double f0, qbar, dface, grad, dsafe, fa, fc;
     bool both, active;
 };
 
-__device__ __forceinline__ Face face_prelim(double el, double er, double hl, double hr, double f0,
-                                            double qbar, double thr)
+__device__ __forceinline__ void face_geom(Face &F, double el, double er, double hl, double hr, double Dl,
+                                          double Dr, double f0, double qbar, double thr)
 {
-    Face F;
     F.f0 = f0;
     F.qbar = qbar;
-    const bool wl = hl + el >= thr, wr = hr + er >= thr;
-    double df = 0.5 * ((hl + el) + (hr + er));
+    const bool wl = Dl >= thr, wr = Dr >= thr;
+    double df = 0.5 * (Dl + Dr);
     double gr = er - el;
-    bool both = wl && wr, active = both;
+    bool active = wl && wr;
+    F.both = active;
     if (wl && !wr) {                        // front_r (kernels.py:191-196)
         const double d_r = el + hr;
         active = d_r >= thr;
@@ -173,27 +195,53 @@ __device__ __forceinline__ Face face_prelim(double el, double er, double hl, dou
     }
     F.dface = df;
     F.grad = gr;
-    F.both = both;
     F.active = active;
-    const double ds = np_max(df, thr);
-    F.dsafe = ds;
-    F.fa = f0 * f0 / ds;                    // fadv
-    F.fc = f0 * (qbar / ds);                // fcross
-    return F;
+    F.dsafe = np_max(df, thr);
 }
 
-// kernels.py:223-247 for one face: upwind advection, friction, update
-__device__ __forceinline__ double face_update(const Face &F, double fa_lo, double fa_hi, double fc_lo,
-                                              double fc_hi, double kfric, double r, double grr)
+// fadv = f0*f0/dsafe, fcross = f0*(qbar/dsafe) with one shared reciprocal
+__device__ __forceinline__ void face_flux(Face &F, bool &ok)
+{
+    const double y = ts_rcp(F.dsafe);
+    F.fa = ts_div(F.f0 * F.f0, F.dsafe, y, ok);
+    F.fc = F.f0 * ts_div(F.qbar, F.dsafe, y, ok);
+}
+
+__device__ __noinline__ double2 face_flux_ieee(double f0, double qbar, double ds)
+{
+    return make_double2(f0 * f0 / ds, f0 * (qbar / ds));
+}
+
+__device__ __forceinline__ double face_adv(const Face &F, double fa_lo, double fa_hi, double fc_lo,
+                                           double fc_hi)
 {
     const double m0 = F.f0, q0 = F.qbar;
     double adv = 0.5 * ((fa_hi - fa_lo) - np_sign(m0) * ((fa_hi + fa_lo) - 2.0 * F.fa));
     adv = adv + 0.5 * ((fc_hi - fc_lo) - np_sign(q0) * ((fc_hi + fc_lo) - 2.0 * F.fc));
-    adv = adv * (F.both ? 1.0 : 0.0);
-    if (!F.active) return 0.0;
-    const double du = F.dsafe;
-    const double fr = kfric * sqrt(m0 * m0 + q0 * q0) / (du * du * ts_cbrt(du));
+    return adv * (F.both ? 1.0 : 0.0);
+}
+
+// kernels.py:235-247: friction, numerator, semi-implicit divide
+__device__ __forceinline__ double face_finish(const Face &F, double adv, double kfric, double r, double grr,
+                                              bool &ok)
+{
+    const double m0 = F.f0, q0 = F.qbar, du = F.dsafe;
+    bool lok = true;
+    const double s = ts_sqrt(m0 * m0 + q0 * q0, lok);
+    const double den = du * du * ts_cbrt(du);
+    const double fr = ts_div(kfric * s, den, ts_rcp(den), lok);
     const double numer = m0 - r * adv - grr * F.dface * F.grad;
+    const double dn = 1.0 + fr;
+    const double v = ts_div(numer, dn, ts_rcp(dn), lok);
+    ok = ok && (lok || !F.active);
+    return F.active ? v : 0.0;
+}
+
+__device__ __noinline__ double face_finish_ieee(double m0, double q0, double du, double dface, double grad,
+                                                double adv, double kfric, double r, double grr)
+{
+    const double fr = kfric * sqrt(m0 * m0 + q0 * q0) / (du * du * ts_cbrt(du));
+    const double numer = m0 - r * adv - grr * dface * grad;
     return numer / (1.0 + fr);
 }
 
@@ -201,7 +249,8 @@ __device__ __forceinline__ double face_update(const Face &F, double fa_lo, doubl
 // r = i0-1 .. i1: prelims of M face r and N row r, then (one row behind)
 // the updates of M face r-1 and N row r-1.  FC_M and FA_N are exchanged
 // across columns through a 3-slot shared ring (one __syncthreads per row);
-// FA_M and FC_N (neighbours along x) stay in registers.
+// FA_M and FC_N (neighbours along x) stay in registers.  The next row's
+// loads are issued before the current row's arithmetic.
 template <int W, int TPC>
 __global__ void __launch_bounds__(32 * W * TPC)
 k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
@@ -236,19 +285,30 @@ k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
     const bool has_nman = B->has_nman != 0;
     const double thr = a.thr, r = B->r, grr = B->grr, kf = B->kf, dtg = B->dtg;
     const int order = B->order;
-
-    // carried registers: previous row (r-1) of column c
-    double e_p = 0.0, h_p = 0.0, Nc_p = 0.0, Nc1_p = 0.0, Mc = 0.0, Mcl = 0.0;
     const int i0 = tl.i0, i1 = tl.i1;
+
+    // row r-1 of column c (carried), and the prefetched row r
+    double e_p = 0.0, h_p = 0.0, D_p = 0.0, Nc_p = 0.0, Nc1_p = 0.0, Mc = 0.0, Mcl = 0.0;
+    double e_n = 0.0, h_n = 0.0, el_n = 0.0, hl_n = 0.0, Nc_n = 0.0, Nc1_n = 0.0, Mn_n = 0.0, Mnl_n = 0.0;
+    size_t rc = (size_t)(i0 - 2 + TS_G) * P + c + TS_G;
     if (colN) {
-        const size_t rp = (size_t)(i0 - 2 + TS_G) * P + c + TS_G;
-        e_p = eta[rp];
-        h_p = hh[rp];
-        Nc_p = no[rp];
-        Nc1_p = no[rp + 1];
-        Mc = mo[rp + P];
-        Mcl = mo[rp + P - 1];
+        e_p = __ldg(eta + rc);
+        h_p = __ldg(hh + rc);
+        Nc_p = __ldg(no + rc);
+        Nc1_p = __ldg(no + rc + 1);
+        Mc = __ldg(mo + rc + P);
+        Mcl = __ldg(mo + rc + P - 1);
+        rc += P;
+        e_n = __ldg(eta + rc);
+        h_n = __ldg(hh + rc);
+        el_n = __ldg(eta + rc - 1);
+        hl_n = __ldg(hh + rc - 1);
+        Nc_n = __ldg(no + rc);
+        Nc1_n = __ldg(no + rc + 1);
+        Mn_n = __ldg(mo + rc + P);
+        Mnl_n = __ldg(mo + rc + P - 1);
     }
+    D_p = h_p + e_p;
     Face Mp{}, Np{};                 // centre faces of row r-1
     double faM_pp = 0.0;             // FA_M(r-2)
     double fcN_pp = 0.0;             // FC_N(r-2)
@@ -256,57 +316,67 @@ k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
         const int rr = i0 - 1 + it;
         const int slot = it % 3, pslot = (it + 2) % 3;
         const bool rowOK = rr <= i1;
-        double e = 0.0, h = 0.0, el = 0.0, hl = 0.0, Nc = 0.0, Nc1 = 0.0, Mn = 0.0, Mnl = 0.0;
-        if (colN && rowOK) {
-            const size_t rc = (size_t)(rr + TS_G) * P + c + TS_G;
-            e = eta[rc];
-            h = hh[rc];
-            el = eta[rc - 1];
-            hl = hh[rc - 1];
-            Nc = no[rc];
-            Nc1 = no[rc + 1];
-            Mn = mo[rc + P];
-            Mnl = mo[rc + P - 1];
+        const double e = e_n, h = h_n, el = el_n, hl = hl_n, Nc = Nc_n, Nc1 = Nc1_n, Mn = Mn_n, Mnl = Mnl_n;
+        if (colN && rr + 1 <= i1) {            // prefetch row rr+1
+            rc += P;
+            e_n = __ldg(eta + rc);
+            h_n = __ldg(hh + rc);
+            el_n = __ldg(eta + rc - 1);
+            hl_n = __ldg(hh + rc - 1);
+            Nc_n = __ldg(no + rc);
+            Nc1_n = __ldg(no + rc + 1);
+            Mn_n = __ldg(mo + rc + P);
+            Mnl_n = __ldg(mo + rc + P - 1);
         }
+        const double D = h + e, Dl = hl + el;
         Face Mf{}, Nf{};
-        if (colM && rowOK && rr <= ni + 1) {
-            // M face rr, column c: cells (rr-1, c) | (rr, c)
-            const double qbar = 0.25 * ((Nc_p + Nc) + (Nc1_p + Nc1));
-            Mf = face_prelim(e_p, e, h_p, h, Mc, qbar, thr);
+        const bool doM = colM && rowOK && rr <= ni + 1;
+        const bool doN = colN && rowOK && rr <= ni;
+        // M face rr, column c: cells (rr-1, c) | (rr, c)
+        face_geom(Mf, e_p, e, h_p, h, D_p, D, Mc, 0.25 * ((Nc_p + Nc) + (Nc1_p + Nc1)), thr);
+        // N face c of row rr: cells (rr, c-1) | (rr, c)
+        face_geom(Nf, el, e, hl, h, Dl, D, Nc, 0.25 * ((Mcl + Mc) + (Mnl + Mn)), thr);
+        bool ok = true;
+        face_flux(Mf, ok);
+        face_flux(Nf, ok);
+        if (!ok) {
+            const double2 fm = face_flux_ieee(Mf.f0, Mf.qbar, Mf.dsafe);
+            const double2 fn = face_flux_ieee(Nf.f0, Nf.qbar, Nf.dsafe);
+            Mf.fa = fm.x; Mf.fc = fm.y;
+            Nf.fa = fn.x; Nf.fc = fn.y;
         }
-        if (colN && rowOK && rr <= ni) {
-            // N face c of row rr: cells (rr, c-1) | (rr, c)
-            const double qbar = 0.25 * ((Mcl + Mc) + (Mnl + Mn));
-            Nf = face_prelim(el, e, hl, h, Nc, qbar, thr);
-        }
+        if (!doM) Mf = Face{};
+        if (!doN) Nf = Face{};
         sFC[slot][tid] = Mf.fc;
         sFA[slot][tid] = Nf.fa;
         __syncthreads();
         if (it >= 2) {
             const int f = rr - 1;
-            if (updM && f < i1) {
-                const double fc_lo = sFC[pslot][tid - 1], fc_hi = sFC[pslot][tid + 1];
-                double kfr = kf;
-                if (has_nman) {
-                    const size_t rc = (size_t)(f + TS_G) * P + c + TS_G;
-                    const double nf = 0.5 * (nman[rc - P] + nman[rc]);
-                    kfr = dtg * nf * nf;
-                }
-                const double v = face_update(Mp, faM_pp, Mf.fa, fc_lo, fc_hi, kfr, r, grr);
-                if (!isfinite(v)) report(a.err, order, 1, f, c);
-                mn[(size_t)(f + TS_G) * P + c + TS_G] = v;
+            const bool dM = updM && f < i1, dN = updN && f < i1 && f < ni;
+            const double advM = face_adv(Mp, faM_pp, Mf.fa, sFC[pslot][tid - 1], sFC[pslot][tid + 1]);
+            const double advN = face_adv(Np, sFA[pslot][tid - 1], sFA[pslot][tid + 1], fcN_pp, Nf.fc);
+            double kM = kf, kN = kf;
+            const size_t fc = (size_t)(f + TS_G) * P + c + TS_G;
+            if (has_nman && (dM || dN)) {
+                const double nfM = 0.5 * (nman[fc - P] + nman[fc]);
+                const double nfN = 0.5 * (nman[fc - 1] + nman[fc]);
+                kM = dtg * nfM * nfM;
+                kN = dtg * nfN * nfN;
             }
-            if (updN && f < i1 && f < ni) {
-                const double fa_lo = sFA[pslot][tid - 1], fa_hi = sFA[pslot][tid + 1];
-                double kfr = kf;
-                if (has_nman) {
-                    const size_t rc = (size_t)(f + TS_G) * P + c + TS_G;
-                    const double nf = 0.5 * (nman[rc - 1] + nman[rc]);
-                    kfr = dtg * nf * nf;
-                }
-                const double v = face_update(Np, fa_lo, fa_hi, fcN_pp, Nf.fc, kfr, r, grr);
-                if (!isfinite(v)) report(a.err, order, 2, f, c);
-                nn[(size_t)(f + TS_G) * P + c + TS_G] = v;
+            bool ok2 = true;
+            double vM = face_finish(Mp, advM, kM, r, grr, ok2);
+            double vN = face_finish(Np, advN, kN, r, grr, ok2);
+            if (!ok2) {
+                vM = Mp.active ? face_finish_ieee(Mp.f0, Mp.qbar, Mp.dsafe, Mp.dface, Mp.grad, advM, kM, r, grr) : 0.0;
+                vN = Np.active ? face_finish_ieee(Np.f0, Np.qbar, Np.dsafe, Np.dface, Np.grad, advN, kN, r, grr) : 0.0;
+            }
+            if (dM) {
+                if (!isfinite(vM)) report(a.err, order, 1, f, c);
+                mn[fc] = vM;
+            }
+            if (dN) {
+                if (!isfinite(vN)) report(a.err, order, 2, f, c);
+                nn[fc] = vN;
             }
         }
         faM_pp = Mp.fa;
@@ -315,6 +385,7 @@ k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
         Np = Nf;
         e_p = e;
         h_p = h;
+        D_p = D;
         Nc_p = Nc;
         Nc1_p = Nc1;
         Mc = Mn;

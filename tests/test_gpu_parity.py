@@ -25,7 +25,10 @@ def _plan(P, system, nr):
     return P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], nr)
 
 
-def assert_same(gpu, orc, where=""):
+def assert_same(gpu, orc, where="", wet="all"):
+    """``wet="interior"`` between mass and halo-eta: the reference refreshes
+    ghost wet flags only when halo-eta writes the ghosts, so until then they
+    describe the previous step (never read in that window)."""
     for bid, o in orc.states.items():
         g = gpu.states[bid]
         for f in FIELDS:
@@ -35,7 +38,10 @@ def assert_same(gpu, orc, where=""):
                 raise AssertionError(f"{where} block {bid} {f}: {len(bad)} cells differ, first "
                                      f"{bad[0].tolist()} gpu={a[tuple(bad[0])]!r} "
                                      f"oracle={b[tuple(bad[0])]!r}")
-        assert np.array_equal(g.wet, o.wet.astype(bool)), (where, bid, "wet")
+        gw, ow = g.wet, o.wet.astype(bool)
+        if wet == "interior":
+            gw, ow = g.interior(gw), o.interior(ow)
+        assert np.array_equal(gw, ow), (where, bid, "wet")
         acc = gpu.accumulators[bid]
         for f in ACCS:
             assert np.array_equal(getattr(acc, f), getattr(o, f), equal_nan=True), (where, bid, f)
@@ -101,7 +107,8 @@ def test_phase_parity(cuda_device, oracle_mod, product, name):
             orc.phase(ph)
             for gph in GPU_PHASES.get(ph, (ph,)):
                 gpu.phase(gph)
-            assert_same(gpu, orc, f"step {step} {ph}")
+            assert_same(gpu, orc, f"step {step} {ph}",
+                        wet="interior" if ph in ("mass", "restrict") else "all")
 
 
 @pytest.mark.parametrize("seed", range(4))
