@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsunami_b200.so")
+LIB_PATH = os.environ.get("TSUNAMI_B200_LIB") or os.path.join(HERE, "libtsunami_b200.so")
 
 TS_OK, TS_ERR_NUMERICS, TS_ERR_CUDA, TS_ERR_INVALID = 0, 1, 2, 3
 ABI_VERSION = 1

@@ -64,8 +64,10 @@ struct ts_handle {
     DevBlock *d_blocks = nullptr;
     char *arena = nullptr;
     size_t arena_bytes = 0;
-    int T = 32;
-    Group groups[4];                      // W = 1..4
+    int T = 34;                           // rows per tile; T + 2 must be a multiple of 3
+    Group groups[4];                      // W = 1..4 (momentum march)
+    Tile *d_all = nullptr;                // every tile (flat mass / fold kernels)
+    int n_all = 0;
     RSeg *d_rseg = nullptr;
     int n_rseg = 0;
     int64_t r_elems = 0;
@@ -126,8 +128,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
         return 0;
     };
     if (mark(0)) return TS_ERR_CUDA;
-    for (auto &gr : h->groups)
-        if (!gr.tiles.empty()) { launch_mass(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, true, s); ++n; }
+    if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
     if (mark(1)) return TS_ERR_CUDA;
     if (h->r_elems) {
         if (h->r_two_pass) {
@@ -170,8 +171,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
 int enqueue_flush(ts_handle *h, cudaStream_t s, int buf)
 {
     const StepArgs a = args_of(h, buf);
-    for (auto &gr : h->groups)
-        if (!gr.tiles.empty()) launch_accumulate(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s);
+    launch_accumulate(a, h->d_all, h->n_all, s);
     CK(cudaGetLastError());
     return TS_OK;
 }
@@ -320,7 +320,11 @@ int create_impl(const ts_desc *d, ts_handle *h)
     h->g = d->gravity;
     h->thr = d->wet_threshold;
     h->nb = d->n_blocks;
-    if (d->tile_rows > 0) h->T = d->tile_rows;
+    if (d->tile_rows > 0) {
+        if ((d->tile_rows + 2) % 3 != 0)
+            return fail(TS_ERR_INVALID, "tile_rows + 2 must be a multiple of 3, got %d", d->tile_rows);
+        h->T = d->tile_rows;
+    }
     CK(cudaSetDevice(h->device));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     for (auto &e : h->ev) CK(cudaEventCreate(&e));
@@ -407,6 +411,12 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     for (auto &gr : h->groups)
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
+    {
+        std::vector<Tile> all;
+        for (auto &gr : h->groups) all.insert(all.end(), gr.tiles.begin(), gr.tiles.end());
+        h->n_all = (int)all.size();
+        if (int rc = upload(&h->d_all, all)) return rc;
+    }
 
     auto owned = [&](int b) { return b >= 0 && b < h->nb && d->blocks[b].owner == h->rank; };
     auto check_blk = [&](int b) { return b >= 0 && b < h->nb; };
@@ -703,10 +713,7 @@ int ts_phase(ts_handle *h, int32_t phase)
     cudaStream_t s = h->stream;
     const StepArgs a = args_of(h, h->cur);
     switch (phase) {
-    case TS_PH_MASS:
-        for (auto &gr : h->groups)
-            if (!gr.tiles.empty()) launch_mass(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
-        break;
+    case TS_PH_MASS: launch_mass(a, h->d_all, h->n_all, false, s); break;
     case TS_PH_RESTRICT:
         if (h->r_two_pass) {
             launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
@@ -822,6 +829,7 @@ void ts_destroy(ts_handle *h)
     for (auto &g : h->graph)
         if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) cudaFree(gr.d);
+    cudaFree(h->d_all);
     cudaFree(h->d_rseg);
     cudaFree(h->d_pseg);
     cudaFree(h->d_heta);

@@ -80,9 +80,8 @@ struct StepArgs {
     const int *acc_flag;            // fold previous step's outputs in K_mass
 };
 
-void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool accumulate,
-                 cudaStream_t s);
-void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
+void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
+void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, int nseg, int64_t nelem, double *stage,
                      int mode, cudaStream_t s);

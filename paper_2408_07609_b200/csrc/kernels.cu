@@ -2,15 +2,16 @@
 //
 // Numerics follow the reference's evaluation order exactly:
 // the file is compiled with -fmad=false (no FMA contraction), IEEE / and
-// sqrt, numpy maximum/sign semantics (np_max / np_sign), and the product's
-// cbrt (cbrt.cuh).  The stored "wet" flags of the reference are derived on
-// the fly as h + eta >= thr, which equals the stored flag at every read site
-// (checked by the parity tests against the oracle, which keeps
-// the explicit array).
+// sqrt (fastmath.cuh replays nvcc's own expansions), numpy maximum/sign
+// semantics (np_max / np_sign), and the product's cbrt (cbrt.cuh).  The
+// reference's stored "wet" flags are derived on the fly as h + eta >= thr,
+// which equals the stored flag at every read site (checked by
+// the parity tests against the oracle, which keeps the explicit array).
 //
 // Kernels:
 //   k_mass      K_mass: continuity (kernels.py:123-155), fused with the
-//               running-maxima fold of the previous step (kernels.py:322-343)
+//               running-maxima fold of the previous step (kernels.py:322-343);
+//               one CTA per tile, one thread per cell (memory-bound)
 //   k_accum     standalone fold (end-of-run flush, kernel-level API)
 //   k_momentum  K_mom: both flux components (kernels.py:158-271) in one
 //               march down each tile's rows; face prelims computed once and
@@ -28,6 +29,8 @@
 
 namespace {
 
+constexpr int kFlatThreads = 256;
+
 __device__ __forceinline__ bool stop_requested(const unsigned long long *err)
 {
     __shared__ int s_stop;
@@ -42,9 +45,8 @@ __device__ __forceinline__ void report(unsigned long long *err, int order, int w
 }
 
 // ------------------------------------------------------------------ mass
-// accumulate_outputs for one cell (kernels.py:327-343); returns false if a
-// batched fast op was out of range (caller redoes it with fold_cell_ieee)
-__device__ __forceinline__ bool fold_cell(const DevBlock *B, size_t ac, double e, double h, double d,
+// accumulate_outputs for one cell (kernels.py:327-343)
+__device__ __forceinline__ void fold_cell(const DevBlock *B, size_t ac, double e, double h, double d,
                                           double Ml, double Mr, double Nl, double Nr, double thr)
 {
     const bool w = d >= thr;
@@ -52,10 +54,13 @@ __device__ __forceinline__ bool fold_cell(const DevBlock *B, size_t ac, double e
     const double nc = 0.5 * (Nl + Nr);
     const double ds = np_max(d, thr);
     bool ok = true;
-    const double y = ts_rcp(ds);
-    const double u = ts_div(mc, ds, y, ok), v = ts_div(nc, ds, y, ok);
-    const double sp = ts_sqrt(u * u + v * v, ok);
-    if (!ok) return false;
+    const TsRcp R = ts_rcp(ds);
+    const double u = ts_div(mc, R, ok), v = ts_div(nc, R, ok);
+    double sp = ts_sqrt(u * u + v * v, ok);
+    if (!ok) {
+        const double uu = mc / ds, vv = nc / ds;
+        sp = sqrt(uu * uu + vv * vv);
+    }
     if (w) {
         const double me = B->acc_eta[ac], nme = np_max(me, e);
         if (!(nme == me || (nme != nme && me != me))) B->acc_eta[ac] = nme;
@@ -66,44 +71,45 @@ __device__ __forceinline__ bool fold_cell(const DevBlock *B, size_t ac, double e
             if (!(nmi == mi || (nmi != nmi && mi != mi))) B->acc_inund[ac] = nmi;
         }
     }
-    return true;
 }
 
-__device__ __noinline__ void fold_cell_ieee(const DevBlock *B, size_t ac, double e, double h, double d,
-                                            double Ml, double Mr, double Nl, double Nr, double thr)
+// Cells of a tile: rows [i0, min(i1, ni)) x columns [j0, min(j1, nj)),
+// visited as a flat index so each thread has several independent cells and
+// all their loads in flight (the kernel is HBM-bound).
+struct CellRange {
+    int i0, j0, ncol, n;
+    float inv;
+};
+
+__device__ __forceinline__ CellRange cell_range(const Tile &tl, int ni, int nj)
 {
-    const bool w = d >= thr;
-    const double mc = 0.5 * (Ml + Mr);
-    const double nc = 0.5 * (Nl + Nr);
-    const double ds = np_max(d, thr);
-    const double u = mc / ds, v = nc / ds;
-    const double sp = sqrt(u * u + v * v);
-    if (w) {
-        B->acc_eta[ac] = np_max(B->acc_eta[ac], e);
-        B->acc_speed[ac] = np_max(B->acc_speed[ac], sp);
-        if (h < 0.0) B->acc_inund[ac] = np_max(B->acc_inund[ac], d);
-    }
+    CellRange c;
+    c.i0 = tl.i0;
+    c.j0 = tl.j0;
+    c.ncol = min(tl.j1, nj) - tl.j0;
+    const int nrow = min(tl.i1, ni) - tl.i0;
+    c.n = (c.ncol > 0 && nrow > 0) ? c.ncol * nrow : 0;
+    c.inv = c.ncol > 0 ? 1.0f / (float)c.ncol : 0.0f;
+    return c;
 }
 
-// One thread per interior column j, marching down rows [i0, i1) of a tile,
-// unrolled so several rows' loads are in flight; M face i of row i+1 is
-// carried in a register.
-template <int W, int TPC, bool FOLD>
-__global__ void __launch_bounds__(32 * W * TPC)
-k_mass(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
+// k -> (row, col) of the range; exact while k < 2^20 (tiles are far smaller)
+__device__ __forceinline__ void cell_of(const CellRange &c, int k, int &i, int &j)
+{
+    const int di = __float2int_rz(((float)k + 0.5f) * c.inv);
+    i = c.i0 + di;
+    j = c.j0 + (k - di * c.ncol);
+}
+
+template <bool FOLD>
+__global__ void __launch_bounds__(kFlatThreads)
+k_mass(StepArgs a, const Tile *__restrict__ tiles)
 {
     if (stop_requested(a.err)) return;
-    const int lt = threadIdx.x / (32 * W), ci = threadIdx.x % (32 * W);
-    const int t = blockIdx.x * TPC + lt;
-    if (t >= ntiles) return;
-    const Tile tl = tiles[t];
+    const Tile tl = tiles[blockIdx.x];
     const DevBlock *B = a.blocks + tl.blk;
-    const int nj = B->nj, ni = B->ni, P = B->P;
-    const int j = tl.j0 + ci;
-    if (j >= tl.j1 || j >= nj) return;
-    const int iend = min(tl.i1, ni);
-    if (tl.i0 >= iend) return;
-    const int cur = a.cur;
+    const CellRange cr = cell_range(tl, B->ni, B->nj);
+    const int P = B->P, cur = a.cur;
     const double *__restrict__ eo = B->eta[cur];
     double *__restrict__ en = B->eta[cur ^ 1];
     const double *__restrict__ mo = B->m[cur];
@@ -111,56 +117,46 @@ k_mass(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
     const double *__restrict__ hh = B->h;
     const double r = B->r, thr = a.thr;
     const bool fold = FOLD && (*a.acc_flag != 0);
-    size_t row = (size_t)(tl.i0 + TS_G) * P + j + TS_G;
-    double Mi = __ldg(mo + row);
+    const int order = B->order;
 #pragma unroll 4
-    for (int i = tl.i0; i < iend; ++i, row += P) {
-        const double Mi1 = __ldg(mo + row + P);
+    for (int k = threadIdx.x; k < cr.n; k += kFlatThreads) {
+        int i, j;
+        cell_of(cr, k, i, j);
+        const size_t row = (size_t)(i + TS_G) * P + j + TS_G;
+        const double Mi = __ldg(mo + row), Mi1 = __ldg(mo + row + P);
         const double Nj = __ldg(no + row), Nj1 = __ldg(no + row + 1);
         const double e0 = __ldg(eo + row), h = __ldg(hh + row);
         const double d = h + e0;
-        if (fold) {
-            // accumulate_outputs of the previous step (kernels.py:322-343):
-            // its eta_new/m_new/n_new are this step's old buffers
-            const size_t ac = (size_t)i * P + j;
-            if (!fold_cell(B, ac, e0, h, d, Mi, Mi1, Nj, Nj1, thr))
-                fold_cell_ieee(B, ac, e0, h, d, Mi, Mi1, Nj, Nj1, thr);
-        }
+        // accumulate_outputs of the previous step (kernels.py:322-343): its
+        // eta_new/m_new/n_new are this step's old buffers
+        if (fold) fold_cell(B, (size_t)i * P + j, e0, h, d, Mi, Mi1, Nj, Nj1, thr);
         // update_mass (kernels.py:134-155); wet_old derived as h + eta_old >= thr
         const double div = r * (Mi1 - Mi) + r * (Nj1 - Nj);
         double e = e0 - div;
         if (!(d >= thr) && div != 0.0) e = np_max(e0, -h) - div;
         if (div != 0.0 && h + e < 0.0) e = -h;
-        if (!isfinite(e)) report(a.err, B->order, 0, i, j);
+        if (!isfinite(e)) report(a.err, order, 0, i, j);
         en[row] = e;
-        Mi = Mi1;
     }
 }
 
 // ------------------------------------------------------ standalone fold
-template <int W, int TPC>
-__global__ void __launch_bounds__(32 * W * TPC)
-k_accum(StepArgs a, const Tile *__restrict__ tiles, int ntiles)
+__global__ void __launch_bounds__(kFlatThreads)
+k_accum(StepArgs a, const Tile *__restrict__ tiles)
 {
     // a.cur names the buffer to read (the "new" role of kernels.py:327-335)
-    const int lt = threadIdx.x / (32 * W), ci = threadIdx.x % (32 * W);
-    const int t = blockIdx.x * TPC + lt;
-    if (t >= ntiles) return;
-    const Tile tl = tiles[t];
+    const Tile tl = tiles[blockIdx.x];
     const DevBlock *B = a.blocks + tl.blk;
-    const int nj = B->nj, ni = B->ni, P = B->P;
-    const int j = tl.j0 + ci;
-    if (j >= tl.j1 || j >= nj) return;
-    const int iend = min(tl.i1, ni);
+    const CellRange cr = cell_range(tl, B->ni, B->nj);
+    const int P = B->P;
     const double *eta = B->eta[a.cur], *m = B->m[a.cur], *n = B->n[a.cur];
-    const double thr = a.thr;
 #pragma unroll 4
-    for (int i = tl.i0; i < iend; ++i) {
-        const size_t row = (size_t)(i + TS_G) * P + j + TS_G, ac = (size_t)i * P + j;
-        const double e = eta[row], h = B->h[row], d = h + e;
-        const double Ml = m[row], Mr = m[row + P], Nl = n[row], Nr = n[row + 1];
-        if (!fold_cell(B, ac, e, h, d, Ml, Mr, Nl, Nr, thr))
-            fold_cell_ieee(B, ac, e, h, d, Ml, Mr, Nl, Nr, thr);
+    for (int k = threadIdx.x; k < cr.n; k += kFlatThreads) {
+        int i, j;
+        cell_of(cr, k, i, j);
+        const size_t row = (size_t)(i + TS_G) * P + j + TS_G;
+        const double e = eta[row], h = B->h[row];
+        fold_cell(B, (size_t)i * P + j, e, h, h + e, m[row], m[row + P], n[row], n[row + 1], a.thr);
     }
 }
 
@@ -182,16 +178,18 @@ __device__ __forceinline__ void face_geom(Face &F, double el, double er, double 
     double gr = er - el;
     bool active = wl && wr;
     F.both = active;
-    if (wl && !wr) {                        // front_r (kernels.py:191-196)
-        const double d_r = el + hr;
-        active = d_r >= thr;
-        df = d_r;
-        gr = np_max(er, -hr) - el;
-    } else if (!wl && wr) {                 // front_l (kernels.py:197-202)
-        const double d_l = er + hl;
-        active = d_l >= thr;
-        df = d_l;
-        gr = er - np_max(el, -hl);
+    if (wl != wr) {
+        if (wl) {                           // front_r (kernels.py:191-196)
+            const double d_r = el + hr;
+            active = d_r >= thr;
+            df = d_r;
+            gr = np_max(er, -hr) - el;
+        } else {                            // front_l (kernels.py:197-202)
+            const double d_l = er + hl;
+            active = d_l >= thr;
+            df = d_l;
+            gr = er - np_max(el, -hl);
+        }
     }
     F.dface = df;
     F.grad = gr;
@@ -199,17 +197,12 @@ __device__ __forceinline__ void face_geom(Face &F, double el, double er, double 
     F.dsafe = np_max(df, thr);
 }
 
-// fadv = f0*f0/dsafe, fcross = f0*(qbar/dsafe) with one shared reciprocal
+// fadv = f0*f0/dsafe, fcross = f0*(qbar/dsafe): one shared reciprocal
 __device__ __forceinline__ void face_flux(Face &F, bool &ok)
 {
-    const double y = ts_rcp(F.dsafe);
-    F.fa = ts_div(F.f0 * F.f0, F.dsafe, y, ok);
-    F.fc = F.f0 * ts_div(F.qbar, F.dsafe, y, ok);
-}
-
-__device__ __noinline__ double2 face_flux_ieee(double f0, double qbar, double ds)
-{
-    return make_double2(f0 * f0 / ds, f0 * (qbar / ds));
+    const TsRcp R = ts_rcp(F.dsafe);
+    F.fa = ts_div(F.f0 * F.f0, R, ok);
+    F.fc = F.f0 * ts_div(F.qbar, R, ok);
 }
 
 __device__ __forceinline__ double face_adv(const Face &F, double fa_lo, double fa_hi, double fc_lo,
@@ -226,15 +219,11 @@ __device__ __forceinline__ double face_finish(const Face &F, double adv, double 
                                               bool &ok)
 {
     const double m0 = F.f0, q0 = F.qbar, du = F.dsafe;
-    bool lok = true;
-    const double s = ts_sqrt(m0 * m0 + q0 * q0, lok);
+    const double s = ts_sqrt(m0 * m0 + q0 * q0, ok);
     const double den = du * du * ts_cbrt(du);
-    const double fr = ts_div(kfric * s, den, ts_rcp(den), lok);
+    const double fr = ts_div(kfric * s, ts_rcp(den), ok);
     const double numer = m0 - r * adv - grr * F.dface * F.grad;
-    const double dn = 1.0 + fr;
-    const double v = ts_div(numer, dn, ts_rcp(dn), lok);
-    ok = ok && (lok || !F.active);
-    return F.active ? v : 0.0;
+    return ts_div(numer, ts_rcp(1.0 + fr), ok);
 }
 
 __device__ __noinline__ double face_finish_ieee(double m0, double q0, double du, double dface, double grad,
@@ -245,19 +234,117 @@ __device__ __noinline__ double face_finish_ieee(double m0, double q0, double du,
     return numer / (1.0 + fr);
 }
 
-// One thread per column c in [j0-1, j1] of a tile; the march visits rows
-// r = i0-1 .. i1: prelims of M face r and N row r, then (one row behind)
-// the updates of M face r-1 and N row r-1.  FC_M and FA_N are exchanged
-// across columns through a 3-slot shared ring (one __syncthreads per row);
-// FA_M and FC_N (neighbours along x) stay in registers.  The next row's
-// loads are issued before the current row's arithmetic.
+// row r of column c as loaded (Mn/Mnl: M faces r+1 at columns c, c-1), plus
+// D = h + eta computed once per cell
+struct RowLd {
+    double e, h, el, hl, Nc, Nc1, Mn, Mnl, D;
+};
+
+struct MomCtx {
+    const double *eta, *hh, *mo, *no, *nman;
+    double *mn, *nn;
+    double *sFC, *sFA;                 // [3][NT] shared rings
+    unsigned long long *err;
+    double thr, r, grr, kf, dtg;
+    int P, ni, nj, c, tid, i0, i1, order, NT;
+    bool colM, colN, updM, updN, has_nman;
+};
+
+__device__ __forceinline__ void load_row(const MomCtx &X, int row, RowLd &L)
+{
+    const size_t rc = (size_t)(row + TS_G) * X.P + X.c + TS_G;
+    L.e = __ldg(X.eta + rc);
+    L.h = __ldg(X.hh + rc);
+    L.el = __ldg(X.eta + rc - 1);
+    L.hl = __ldg(X.hh + rc - 1);
+    L.Nc = __ldg(X.no + rc);
+    L.Nc1 = __ldg(X.no + rc + 1);
+    L.Mn = __ldg(X.mo + rc + X.P);
+    L.Mnl = __ldg(X.mo + rc + X.P - 1);
+}
+
+// One march step at row rr (iteration it): prelims of M face rr and N row
+// rr from rows rr-1 (Lp) and rr (Lc), then the updates of M face rr-1 and
+// N row rr-1 (their centre faces in FpM/FpN, FA_M/FC_N of row rr-2 in
+// Fpp_M/Fpp_N).  Lf receives the prefetch of row rr+1; SLOT is the
+// compile-time shared-ring slot of row rr.
+template <int SLOT>
+__device__ __forceinline__ void mom_step(const MomCtx &X, int it, const RowLd &Lp, RowLd &Lc, RowLd &Lf,
+                                         const Face &Fpp_M, const Face &Fpp_N, const Face &FpM,
+                                         const Face &FpN, Face &FcM, Face &FcN)
+{
+    constexpr int PSLOT = (SLOT + 2) % 3;
+    const int rr = X.i0 - 1 + it;
+    const bool rowOK = rr <= X.i1;
+    if (X.colN && rr + 1 <= X.i1) load_row(X, rr + 1, Lf);
+    Lc.D = Lc.h + Lc.e;
+    // M face rr, column c: cells (rr-1, c) | (rr, c); Mc = M(rr, c) = Lp.Mn
+    face_geom(FcM, Lp.e, Lc.e, Lp.h, Lc.h, Lp.D, Lc.D, Lp.Mn,
+              0.25 * ((Lp.Nc + Lc.Nc) + (Lp.Nc1 + Lc.Nc1)), X.thr);
+    // N face c of row rr: cells (rr, c-1) | (rr, c)
+    face_geom(FcN, Lc.el, Lc.e, Lc.hl, Lc.h, Lc.hl + Lc.el, Lc.D, Lc.Nc,
+              0.25 * ((Lp.Mnl + Lp.Mn) + (Lc.Mnl + Lc.Mn)), X.thr);
+    bool ok = true;
+    face_flux(FcM, ok);
+    face_flux(FcN, ok);
+    if (!ok) {
+        FcM.fa = FcM.f0 * FcM.f0 / FcM.dsafe;
+        FcM.fc = FcM.f0 * (FcM.qbar / FcM.dsafe);
+        FcN.fa = FcN.f0 * FcN.f0 / FcN.dsafe;
+        FcN.fc = FcN.f0 * (FcN.qbar / FcN.dsafe);
+    }
+    X.sFC[SLOT * X.NT + X.tid] = FcM.fc;
+    X.sFA[SLOT * X.NT + X.tid] = FcN.fa;
+    __syncthreads();
+    if (it < 2) return;
+    const int f = rr - 1;
+    const bool dM = X.updM && f < X.i1 && rowOK;
+    const bool dN = X.updN && f < X.i1 && f < X.ni && rowOK;
+    const double advM = face_adv(FpM, Fpp_M.fa, FcM.fa, X.sFC[PSLOT * X.NT + X.tid - 1],
+                                 X.sFC[PSLOT * X.NT + X.tid + 1]);
+    const double advN = face_adv(FpN, X.sFA[PSLOT * X.NT + X.tid - 1], X.sFA[PSLOT * X.NT + X.tid + 1],
+                                 Fpp_N.fc, FcN.fc);
+    double kM = X.kf, kN = X.kf;
+    const size_t fc = (size_t)(f + TS_G) * X.P + X.c + TS_G;
+    if (X.has_nman && (dM || dN)) {
+        const double nfM = 0.5 * (X.nman[fc - X.P] + X.nman[fc]);
+        const double nfN = 0.5 * (X.nman[fc - 1] + X.nman[fc]);
+        kM = X.dtg * nfM * nfM;
+        kN = X.dtg * nfN * nfN;
+    }
+    bool okM = true, okN = true;
+    double vM = face_finish(FpM, advM, kM, X.r, X.grr, okM);
+    double vN = face_finish(FpN, advN, kN, X.r, X.grr, okN);
+    if (!((okM || !FpM.active) && (okN || !FpN.active))) {
+        vM = face_finish_ieee(FpM.f0, FpM.qbar, FpM.dsafe, FpM.dface, FpM.grad, advM, kM, X.r, X.grr);
+        vN = face_finish_ieee(FpN.f0, FpN.qbar, FpN.dsafe, FpN.dface, FpN.grad, advN, kN, X.r, X.grr);
+    }
+    if (dM) {
+        const double v = FpM.active ? vM : 0.0;
+        if (!isfinite(v)) report(X.err, X.order, 1, f, X.c);
+        X.mn[fc] = v;
+    }
+    if (dN) {
+        const double v = FpN.active ? vN : 0.0;
+        if (!isfinite(v)) report(X.err, X.order, 2, f, X.c);
+        X.nn[fc] = v;
+    }
+}
+
+// One thread per column c in [j0-1, j1] of a tile (W warps per tile, TPC
+// tiles per CTA); the march visits rows r = i0-1 .. i0+T (T+2 a multiple of
+// 3).  Unrolled by 3 so load buffers, face sets and shared-ring slots rotate
+// by renaming only.
+#ifndef TS_MOM_MINB
+#define TS_MOM_MINB 1
+#endif
 template <int W, int TPC>
-__global__ void __launch_bounds__(32 * W * TPC)
+__global__ void __launch_bounds__(32 * W * TPC, TS_MOM_MINB)
 k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
 {
     constexpr int NT = 32 * W * TPC;
-    __shared__ double sFC[3][NT];
-    __shared__ double sFA[3][NT];
+    __shared__ double sFC[3 * NT];
+    __shared__ double sFA[3 * NT];
     if (stop_requested(a.err)) return;
     const int tid = threadIdx.x;
     const int lt = tid / (32 * W), ci = tid % (32 * W);
@@ -267,129 +354,51 @@ k_momentum(StepArgs a, const Tile *__restrict__ tiles, int ntiles, int T)
     if (tv) tl = tiles[t];
     else tl = Tile{0, 0, 0, 0, 0, 0};
     const DevBlock *B = a.blocks + tl.blk;
-    const int ni = B->ni, nj = B->nj, P = B->P;
-    const int c = tl.j0 - 1 + ci;
-    const bool inTile = tv && c <= tl.j1;
-    const bool colM = inTile && c <= nj;          // M window columns -1..nj
-    const bool colN = inTile && c <= nj + 1;      // N window faces -1..nj+1
-    const bool updM = tv && c >= tl.j0 && c < tl.j1 && c < nj;
-    const bool updN = tv && c >= tl.j0 && c < tl.j1 && c <= nj;
+    MomCtx X;
+    X.ni = B->ni;
+    X.nj = B->nj;
+    X.P = B->P;
+    X.c = tl.j0 - 1 + ci;
+    const bool inTile = tv && X.c <= tl.j1;
+    X.colM = inTile && X.c <= X.nj;               // M window columns -1..nj
+    X.colN = inTile && X.c <= X.nj + 1;           // N window faces -1..nj+1
+    X.updM = tv && X.c >= tl.j0 && X.c < tl.j1 && X.c < X.nj;
+    X.updN = tv && X.c >= tl.j0 && X.c < tl.j1 && X.c <= X.nj;
     const int cur = a.cur;
-    const double *__restrict__ eta = B->eta[cur ^ 1];
-    const double *__restrict__ hh = B->h;
-    const double *__restrict__ mo = B->m[cur];
-    const double *__restrict__ no = B->n[cur];
-    double *__restrict__ mn = B->m[cur ^ 1];
-    double *__restrict__ nn = B->n[cur ^ 1];
-    const double *__restrict__ nman = B->nman;
-    const bool has_nman = B->has_nman != 0;
-    const double thr = a.thr, r = B->r, grr = B->grr, kf = B->kf, dtg = B->dtg;
-    const int order = B->order;
-    const int i0 = tl.i0, i1 = tl.i1;
+    X.eta = B->eta[cur ^ 1];
+    X.hh = B->h;
+    X.mo = B->m[cur];
+    X.no = B->n[cur];
+    X.mn = B->m[cur ^ 1];
+    X.nn = B->n[cur ^ 1];
+    X.nman = B->nman;
+    X.has_nman = B->has_nman != 0;
+    X.thr = a.thr;
+    X.r = B->r;
+    X.grr = B->grr;
+    X.kf = B->kf;
+    X.dtg = B->dtg;
+    X.order = B->order;
+    X.err = a.err;
+    X.sFC = sFC;
+    X.sFA = sFA;
+    X.tid = tid;
+    X.NT = NT;
+    X.i0 = tl.i0;
+    X.i1 = tl.i1;
 
-    // row r-1 of column c (carried), and the prefetched row r
-    double e_p = 0.0, h_p = 0.0, D_p = 0.0, Nc_p = 0.0, Nc1_p = 0.0, Mc = 0.0, Mcl = 0.0;
-    double e_n = 0.0, h_n = 0.0, el_n = 0.0, hl_n = 0.0, Nc_n = 0.0, Nc1_n = 0.0, Mn_n = 0.0, Mnl_n = 0.0;
-    size_t rc = (size_t)(i0 - 2 + TS_G) * P + c + TS_G;
-    if (colN) {
-        e_p = __ldg(eta + rc);
-        h_p = __ldg(hh + rc);
-        Nc_p = __ldg(no + rc);
-        Nc1_p = __ldg(no + rc + 1);
-        Mc = __ldg(mo + rc + P);
-        Mcl = __ldg(mo + rc + P - 1);
-        rc += P;
-        e_n = __ldg(eta + rc);
-        h_n = __ldg(hh + rc);
-        el_n = __ldg(eta + rc - 1);
-        hl_n = __ldg(hh + rc - 1);
-        Nc_n = __ldg(no + rc);
-        Nc1_n = __ldg(no + rc + 1);
-        Mn_n = __ldg(mo + rc + P);
-        Mnl_n = __ldg(mo + rc + P - 1);
+    RowLd L0{}, L1{}, L2{};
+    Face A0{}, A1{}, A2{}, B0{}, B1{}, B2{};      // M / N face sets
+    if (X.colN) {
+        load_row(X, X.i0 - 2, L2);                // row i0-2 (prev of the first step)
+        load_row(X, X.i0 - 1, L0);                // row i0-1 (first step)
     }
-    D_p = h_p + e_p;
-    Face Mp{}, Np{};                 // centre faces of row r-1
-    double faM_pp = 0.0;             // FA_M(r-2)
-    double fcN_pp = 0.0;             // FC_N(r-2)
-    for (int it = 0; it < T + 2; ++it) {
-        const int rr = i0 - 1 + it;
-        const int slot = it % 3, pslot = (it + 2) % 3;
-        const bool rowOK = rr <= i1;
-        const double e = e_n, h = h_n, el = el_n, hl = hl_n, Nc = Nc_n, Nc1 = Nc1_n, Mn = Mn_n, Mnl = Mnl_n;
-        if (colN && rr + 1 <= i1) {            // prefetch row rr+1
-            rc += P;
-            e_n = __ldg(eta + rc);
-            h_n = __ldg(hh + rc);
-            el_n = __ldg(eta + rc - 1);
-            hl_n = __ldg(hh + rc - 1);
-            Nc_n = __ldg(no + rc);
-            Nc1_n = __ldg(no + rc + 1);
-            Mn_n = __ldg(mo + rc + P);
-            Mnl_n = __ldg(mo + rc + P - 1);
-        }
-        const double D = h + e, Dl = hl + el;
-        Face Mf{}, Nf{};
-        const bool doM = colM && rowOK && rr <= ni + 1;
-        const bool doN = colN && rowOK && rr <= ni;
-        // M face rr, column c: cells (rr-1, c) | (rr, c)
-        face_geom(Mf, e_p, e, h_p, h, D_p, D, Mc, 0.25 * ((Nc_p + Nc) + (Nc1_p + Nc1)), thr);
-        // N face c of row rr: cells (rr, c-1) | (rr, c)
-        face_geom(Nf, el, e, hl, h, Dl, D, Nc, 0.25 * ((Mcl + Mc) + (Mnl + Mn)), thr);
-        bool ok = true;
-        face_flux(Mf, ok);
-        face_flux(Nf, ok);
-        if (!ok) {
-            const double2 fm = face_flux_ieee(Mf.f0, Mf.qbar, Mf.dsafe);
-            const double2 fn = face_flux_ieee(Nf.f0, Nf.qbar, Nf.dsafe);
-            Mf.fa = fm.x; Mf.fc = fm.y;
-            Nf.fa = fn.x; Nf.fc = fn.y;
-        }
-        if (!doM) Mf = Face{};
-        if (!doN) Nf = Face{};
-        sFC[slot][tid] = Mf.fc;
-        sFA[slot][tid] = Nf.fa;
-        __syncthreads();
-        if (it >= 2) {
-            const int f = rr - 1;
-            const bool dM = updM && f < i1, dN = updN && f < i1 && f < ni;
-            const double advM = face_adv(Mp, faM_pp, Mf.fa, sFC[pslot][tid - 1], sFC[pslot][tid + 1]);
-            const double advN = face_adv(Np, sFA[pslot][tid - 1], sFA[pslot][tid + 1], fcN_pp, Nf.fc);
-            double kM = kf, kN = kf;
-            const size_t fc = (size_t)(f + TS_G) * P + c + TS_G;
-            if (has_nman && (dM || dN)) {
-                const double nfM = 0.5 * (nman[fc - P] + nman[fc]);
-                const double nfN = 0.5 * (nman[fc - 1] + nman[fc]);
-                kM = dtg * nfM * nfM;
-                kN = dtg * nfN * nfN;
-            }
-            bool ok2 = true;
-            double vM = face_finish(Mp, advM, kM, r, grr, ok2);
-            double vN = face_finish(Np, advN, kN, r, grr, ok2);
-            if (!ok2) {
-                vM = Mp.active ? face_finish_ieee(Mp.f0, Mp.qbar, Mp.dsafe, Mp.dface, Mp.grad, advM, kM, r, grr) : 0.0;
-                vN = Np.active ? face_finish_ieee(Np.f0, Np.qbar, Np.dsafe, Np.dface, Np.grad, advN, kN, r, grr) : 0.0;
-            }
-            if (dM) {
-                if (!isfinite(vM)) report(a.err, order, 1, f, c);
-                mn[fc] = vM;
-            }
-            if (dN) {
-                if (!isfinite(vN)) report(a.err, order, 2, f, c);
-                nn[fc] = vN;
-            }
-        }
-        faM_pp = Mp.fa;
-        fcN_pp = Np.fc;
-        Mp = Mf;
-        Np = Nf;
-        e_p = e;
-        h_p = h;
-        D_p = D;
-        Nc_p = Nc;
-        Nc1_p = Nc1;
-        Mc = Mn;
-        Mcl = Mnl;
+    L2.D = L2.h + L2.e;
+    // step k: current row in L[k%3], prev in L[(k+2)%3], prefetch into L[(k+1)%3]
+    for (int it = 0; it < T + 2; it += 3) {
+        mom_step<0>(X, it, L2, L0, L1, A1, B1, A2, B2, A0, B0);
+        mom_step<1>(X, it + 1, L0, L1, L2, A2, B2, A0, B0, A1, B1);
+        mom_step<2>(X, it + 2, L1, L2, L0, A0, B0, A1, B1, A2, B2);
     }
 }
 
@@ -514,43 +523,17 @@ constexpr int tiles_per_cta() { return W == 1 ? 4 : (W == 2 ? 2 : 1); }
 }  // namespace
 
 // ------------------------------------------------------------- launchers
-void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fold,
-                 cudaStream_t s)
+void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool fold, cudaStream_t s)
 {
-    (void)T;
     if (ntiles <= 0) return;
-#define TS_MASS(WW)                                                                         \
-    {                                                                                       \
-        constexpr int TPC = tiles_per_cta<WW>();                                            \
-        const int grid = (ntiles + TPC - 1) / TPC;                                          \
-        if (fold) k_mass<WW, TPC, true><<<grid, 32 * WW * TPC, 0, s>>>(a, tiles, ntiles);   \
-        else k_mass<WW, TPC, false><<<grid, 32 * WW * TPC, 0, s>>>(a, tiles, ntiles);       \
-    }
-    switch (W) {
-    case 1: TS_MASS(1); break;
-    case 2: TS_MASS(2); break;
-    case 3: TS_MASS(3); break;
-    default: TS_MASS(4); break;
-    }
-#undef TS_MASS
+    if (fold) k_mass<true><<<ntiles, kFlatThreads, 0, s>>>(a, tiles);
+    else k_mass<false><<<ntiles, kFlatThreads, 0, s>>>(a, tiles);
 }
 
-void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s)
+void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s)
 {
-    (void)T;
     if (ntiles <= 0) return;
-#define TS_ACC(WW)                                                                          \
-    {                                                                                       \
-        constexpr int TPC = tiles_per_cta<WW>();                                            \
-        k_accum<WW, TPC><<<(ntiles + TPC - 1) / TPC, 32 * WW * TPC, 0, s>>>(a, tiles, ntiles); \
-    }
-    switch (W) {
-    case 1: TS_ACC(1); break;
-    case 2: TS_ACC(2); break;
-    case 3: TS_ACC(3); break;
-    default: TS_ACC(4); break;
-    }
-#undef TS_ACC
+    k_accum<<<ntiles, kFlatThreads, 0, s>>>(a, tiles);
 }
 
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s)
