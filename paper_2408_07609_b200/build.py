@@ -12,7 +12,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "libtsunami_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("kernels.cu", "api.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("step_kernels.cu", "api.cu")]
 DEPS = SOURCES + [os.path.join(HERE, "csrc", f) for f in ("common.cuh", "cbrt.cuh", "fastmath.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "tsunami_b200.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
