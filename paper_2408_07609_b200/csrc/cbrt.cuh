@@ -36,6 +36,24 @@ TS_HD uint64_t ts_bits(double x) { uint64_t b; std::memcpy(&b, &x, 8); return b;
 TS_HD double ts_from_bits(uint64_t b) { double x; std::memcpy(&x, &b, 8); return x; }
 #endif
 
+// polynomial coefficients c7..c0, 2^(-r/3) for r = 0, 1, 2, and 1/3.  The
+// device reads them from the constant bank (a DFMA operand) instead of
+// rematerialising each 64-bit literal with two uniform moves per use.
+#define TS_CBRT_TABLE                                                                 \
+    -0x1.9975209200000p-8, 0x1.36f21412b8c00p-4, -0x1.9bda02c244c00p-2,                \
+    0x1.378ae90591ba8p+0, -0x1.283918219a43ep+1, 0x1.704716488edf7p+1,                 \
+    -0x1.34eeb196c1ab5p+1, 0x1.f7574f9197f7cp+0, 0x1.0p+0, 0x1.965fea53d6e3dp-1,       \
+    0x1.428a2f98d728bp-1, 0x1.5555555555555p-2
+#if defined(__CUDACC__)
+static __constant__ double ts_cbrt_k_dev[12] = {TS_CBRT_TABLE};
+#endif
+static const double ts_cbrt_k_host[12] = {TS_CBRT_TABLE};
+#if defined(__CUDA_ARCH__)
+#define TS_CBRT_K(i) ts_cbrt_k_dev[i]
+#else
+#define TS_CBRT_K(i) ts_cbrt_k_host[i]
+#endif
+
 TS_HD double ts_cbrt_pos_normal(double x, int extra_exp)
 {
     const uint64_t b = ts_bits(x);
@@ -44,16 +62,16 @@ TS_HD double ts_cbrt_pos_normal(double x, int extra_exp)
     const int q = (e >= 0) ? e / 3 : -((2 - e) / 3);
     const int r = e - 3 * q;
     const double t = TS_MUL(m, (double)(1 << r));
-    double p = -0x1.9975209200000p-8;
-    p = TS_FMA(p, m, 0x1.36f21412b8c00p-4);
-    p = TS_FMA(p, m, -0x1.9bda02c244c00p-2);
-    p = TS_FMA(p, m, 0x1.378ae90591ba8p+0);
-    p = TS_FMA(p, m, -0x1.283918219a43ep+1);
-    p = TS_FMA(p, m, 0x1.704716488edf7p+1);
-    p = TS_FMA(p, m, -0x1.34eeb196c1ab5p+1);
-    p = TS_FMA(p, m, 0x1.f7574f9197f7cp+0);
-    const double c3 = (r == 0) ? 0x1.0p+0 : ((r == 1) ? 0x1.965fea53d6e3dp-1 : 0x1.428a2f98d728bp-1);
-    const double third = 0x1.5555555555555p-2;
+    double p = TS_CBRT_K(0);
+    p = TS_FMA(p, m, TS_CBRT_K(1));
+    p = TS_FMA(p, m, TS_CBRT_K(2));
+    p = TS_FMA(p, m, TS_CBRT_K(3));
+    p = TS_FMA(p, m, TS_CBRT_K(4));
+    p = TS_FMA(p, m, TS_CBRT_K(5));
+    p = TS_FMA(p, m, TS_CBRT_K(6));
+    p = TS_FMA(p, m, TS_CBRT_K(7));
+    const double c3 = TS_CBRT_K(8 + r);
+    const double third = TS_CBRT_K(11);
     double R = TS_MUL(p, c3);
     const double R3 = TS_MUL(TS_MUL(R, R), R);
     const double en = TS_FMA(-t, R3, 1.0);
