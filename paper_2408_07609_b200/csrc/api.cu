@@ -68,6 +68,8 @@ struct ts_handle {
     Group groups[4];                      // W = 1..4 (momentum march)
     Tile *d_all = nullptr;                // every tile (flat mass / fold kernels)
     int n_all = 0;
+    Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
+    int n_perim = 0;
     RSeg *d_rseg = nullptr;
     int n_rseg = 0;
     int64_t r_elems = 0;
@@ -81,9 +83,13 @@ struct ts_handle {
     bool edge_serial = false;
     double *d_stage = nullptr;
     unsigned long long *d_err = nullptr;
+    unsigned long long *d_err_next = nullptr;
     int *d_accflag = nullptr;
-    cudaGraph_t graph[2] = {nullptr, nullptr};          // kept: exec node updates refer to them
-    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    // step graphs per variant (bit 0: full mass pass instead of perimeter
+    // pass; bit 1: momentum fused with the next step's interior mass) and
+    // buffer parity; kept alive because exec event-node updates refer to them
+    cudaGraph_t graph[4][2] = {};
+    cudaGraphExec_t gexec[4][2] = {};
     cudaEvent_t ev[kPhaseEvents] = {};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     int cur = 0;
@@ -93,7 +99,7 @@ struct ts_handle {
     double mass_s = 0, mom_s = 0, step_s = 0;
     int launches = 0;
     bool timing = false;
-    cudaGraphNode_t ev_node[2][kPhaseEvents] = {};   // per parity graph
+    cudaGraphNode_t ev_node[4][2][kPhaseEvents] = {};
     std::vector<cudaEvent_t> pool;                    // 5 per timed step
 };
 
@@ -106,14 +112,22 @@ StepArgs args_of(const ts_handle *h, int cur)
     a.cur = cur;
     a.thr = h->thr;
     a.err = h->d_err;
+    a.err_next = h->d_err_next;
     a.acc_flag = h->d_accflag;
     return a;
 }
 
+enum { kMassAll = 1, kFuse = 2 };
+
 // The step body, in the reference's phase order (runner.py:352-365).  When
 // `events` the phase boundaries are recorded (external event nodes when
-// captured into a graph).
-int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunch)
+// captured into a graph).  `variant`: kMassAll runs the continuity update on
+// every cell (first step of a run call), otherwise only on the perimeter
+// cells the previous fused momentum kernel left; kFuse makes this step's
+// momentum kernel also advance the interior cells' water level of the next
+// step (never on the last step of a run call, so the state at return is
+// exactly the reference's).
+int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events, int *nlaunch)
 {
     const StepArgs a = args_of(h, cur);
     int n = 0;
@@ -128,7 +142,13 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
         return 0;
     };
     if (mark(0)) return TS_ERR_CUDA;
-    if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
+    if (variant & kMassAll) {
+        if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
+    } else {
+        launch_promote(a, s);
+        ++n;
+        if (h->n_perim) { launch_mass(a, h->d_perim, h->n_perim, true, s); ++n; }
+    }
     if (mark(1)) return TS_ERR_CUDA;
     if (h->r_elems) {
         if (h->r_two_pass) {
@@ -144,7 +164,10 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
     if (mark(3)) return TS_ERR_CUDA;
     for (auto &gr : h->groups)
-        if (!gr.tiles.empty()) { launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s); ++n; }
+        if (!gr.tiles.empty()) {
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, s);
+            ++n;
+        }
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
     if (mark(5)) return TS_ERR_CUDA;
@@ -176,20 +199,23 @@ int enqueue_flush(ts_handle *h, cudaStream_t s, int buf)
     return TS_OK;
 }
 
-int build_graphs(ts_handle *h)
+// capture (once) and return the executable graph of a step variant/parity
+int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
 {
-    for (int c = 0; c < 2; ++c) {
+    if (!h->gexec[variant][c]) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-        int rc = enqueue_step(h, h->stream, c, true, &h->launches);
+        int nl = 0;
+        int rc = enqueue_step(h, h->stream, c, variant, true, &nl);
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         if (rc) return rc;
         if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        if (variant == kFuse) h->launches = nl;
         size_t nn = 0;
         CK(cudaGraphGetNodes(g, nullptr, &nn));
         std::vector<cudaGraphNode_t> nodes(nn);
         CK(cudaGraphGetNodes(g, nodes.data(), &nn));
-        CK(cudaGraphInstantiate(&h->gexec[c], g, 0));
+        CK(cudaGraphInstantiate(&h->gexec[variant][c], g, 0));
         for (auto nd : nodes) {
             cudaGraphNodeType ty;
             CK(cudaGraphNodeGetType(nd, &ty));
@@ -197,10 +223,11 @@ int build_graphs(ts_handle *h)
             cudaEvent_t ev;
             CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
             for (int k = 0; k < kPhaseEvents; ++k)
-                if (ev == h->ev[k]) h->ev_node[c][k] = nd;
+                if (ev == h->ev[k]) h->ev_node[variant][c][k] = nd;
         }
-        h->graph[c] = g;
+        h->graph[variant][c] = g;
     }
+    *out = h->gexec[variant][c];
     return TS_OK;
 }
 
@@ -393,10 +420,20 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
     CK(cudaMalloc((void **)&h->d_err, sizeof(unsigned long long)));
     CK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
+    CK(cudaMalloc((void **)&h->d_err_next, sizeof(unsigned long long)));
+    CK(cudaMemset(h->d_err_next, 0xff, sizeof(unsigned long long)));
     CK(cudaMalloc((void **)&h->d_accflag, sizeof(int)));
     CK(cudaMemset(h->d_accflag, 0, sizeof(int)));
 
-    // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1)
+    // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1); pad = end of
+    // the fused-mass columns (interior, minus a column-tile boundary column,
+    // whose N face j1 belongs to the next column tile)
+    std::vector<Tile> perim;
+    auto add_rect = [&](int b, int i0, int i1, int j0, int j1) {
+        for (int ia = i0; ia < i1; ia += 1024)
+            for (int ja = j0; ja < j1; ja += 4096)
+                perim.push_back(Tile{b, ia, std::min(ia + 1024, i1), ja, std::min(ja + 4096, j1), 0});
+    };
     for (int k = 0; k < 4; ++k) h->groups[k].W = k + 1;
     for (int b = 0; b < h->nb; ++b) {
         if (d->blocks[b].owner != h->rank) continue;
@@ -404,10 +441,25 @@ int create_impl(const ts_desc *d, ts_handle *h)
         int W, w;
         if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
         else { W = 4; w = 126; }
-        for (int j0 = 0; j0 < nj + 1; j0 += w)
+        std::vector<int> cut_cols;
+        for (int j0 = 0; j0 < nj + 1; j0 += w) {
+            const int j1 = std::min(j0 + w, nj + 1);
+            const int mj1 = j1 == nj + 1 ? nj - 1 : j1 - 1;
+            if (j1 != nj + 1 && j1 - 1 >= 1 && j1 - 1 <= nj - 2) cut_cols.push_back(j1 - 1);
             for (int i0 = 0; i0 < ni + 1; i0 += h->T)
-                h->groups[W - 1].tiles.push_back(
-                    Tile{b, i0, std::min(i0 + h->T, ni + 1), j0, std::min(j0 + w, nj + 1), 0});
+                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + h->T, ni + 1), j0, j1, mj1});
+        }
+        // cells the fused kernel does not advance: rows 0 and ni-1, columns
+        // 0 and nj-1, and column-tile boundary columns
+        if (ni <= 2 || nj <= 2) {
+            add_rect(b, 0, ni, 0, nj);
+        } else {
+            add_rect(b, 0, 1, 0, nj);
+            add_rect(b, ni - 1, ni, 0, nj);
+            add_rect(b, 1, ni - 1, 0, 1);
+            add_rect(b, 1, ni - 1, nj - 1, nj);
+            for (int cc : cut_cols) add_rect(b, 1, ni - 1, cc, cc + 1);
+        }
     }
     for (auto &gr : h->groups)
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
@@ -416,6 +468,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
         for (auto &gr : h->groups) all.insert(all.end(), gr.tiles.begin(), gr.tiles.end());
         h->n_all = (int)all.size();
         if (int rc = upload(&h->d_all, all)) return rc;
+        h->n_perim = (int)perim.size();
+        if (int rc = upload(&h->d_perim, perim)) return rc;
     }
 
     auto owned = [&](int b) { return b >= 0 && b < h->nb && d->blocks[b].owner == h->rank; };
@@ -573,7 +627,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
     CK(cudaDeviceSynchronize());
-    return build_graphs(h);
+    cudaGraphExec_t g;
+    return get_graph(h, kFuse, 0, &g);
 }
 
 int check_error(ts_handle *h)
@@ -619,20 +674,27 @@ int ts_run(ts_handle *h, int64_t n_steps)
     if (int rc = check_error(h)) return rc;
     if (n_steps == 0) return TS_OK;
     cudaStream_t s = h->stream;
-    int64_t done = 0;
-    // the first step of this call runs eagerly with phase events: its
-    // per-phase times apportion the run's device time to the routines
-    // (runner.ROUTINES); the fold flag is cleared for the very first step
-    // of the simulation (no previous outputs exist yet)
+    // step k of this call: the first runs the full continuity pass, the
+    // others only the perimeter cells the previous (fused) momentum kernel
+    // left; every step but the last fuses the next step's interior mass
+    auto variant_of = [&](int64_t k) {
+        return (k == 0 ? kMassAll : 0) | (k + 1 < n_steps ? kFuse : 0);
+    };
+    // the fold flag is cleared for the very first step of the simulation
+    // (no previous outputs exist yet)
     if (h->steps == 0) CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
     CK(cudaEventRecord(h->t0, s));
-    if (int rc = enqueue_step(h, s, h->cur, true, nullptr)) return rc;
+    // first step: its phase events apportion the call's device time to the
+    // routines (runner.ROUTINES)
+    cudaGraphExec_t g;
+    if (int rc = get_graph(h, variant_of(0), h->cur, &g)) return rc;
+    CK(cudaGraphLaunch(g, s));
     float ph[7] = {0};
     CK(cudaEventSynchronize(h->ev[kPhaseEvents - 1]));
     for (int k = 0; k < 7; ++k) CK(cudaEventElapsedTime(&ph[k], h->ev[k], h->ev[k + 1]));
     h->cur ^= 1;
     h->steps += 1;
-    done = 1;
+    int64_t done = 1;
     CK(cudaMemsetAsync(h->d_accflag, 1, 1, s));
     const int64_t chunk = 256;
     double sum_mass = 0, sum_mom = 0, sum_step = 0;
@@ -645,11 +707,15 @@ int ts_run(ts_handle *h, int64_t n_steps)
             for (size_t k = old; k < h->pool.size(); ++k) CK(cudaEventCreate(&h->pool[k]));
         }
         for (int64_t k = 0; k < n; ++k) {
+            const int v = variant_of(done + k);
+            if (int rc = get_graph(h, v, h->cur, &g)) return rc;
             if (h->timing)
                 for (int q = 0; q < 5; ++q)
-                    CK(cudaGraphExecEventRecordNodeSetEvent(h->gexec[h->cur], h->ev_node[h->cur][kTimed[q]],
-                                                            h->pool[5 * k + q]));
-            CK(cudaGraphLaunch(h->gexec[h->cur], s));
+                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[v][h->cur][kTimed[q]], h->pool[5 * k + q]));
+            CK(cudaGraphLaunch(g, s));
+            if (h->timing)    // leave the graph's own phase events in place
+                for (int q = 0; q < 5; ++q)
+                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[v][h->cur][kTimed[q]], h->ev[kTimed[q]]));
             h->cur ^= 1;
         }
         h->steps += n;
@@ -667,10 +733,6 @@ int ts_run(ts_handle *h, int64_t n_steps)
                 sum_mass += a; sum_mom += b; sum_step += c;
             }
             timed += n;
-            // restore the graphs' own phase events
-            for (int c = 0; c < 2; ++c)
-                for (int q = 0; q < 5; ++q)
-                    CK(cudaGraphExecEventRecordNodeSetEvent(h->gexec[c], h->ev_node[c][kTimed[q]], h->ev[kTimed[q]]));
         }
     }
     if (timed) {
@@ -725,7 +787,7 @@ int ts_phase(ts_handle *h, int32_t phase)
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
     case TS_PH_MOMENTUM:
         for (auto &gr : h->groups)
-            if (!gr.tiles.empty()) launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, s);
+            if (!gr.tiles.empty()) launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
     case TS_PH_PROLONG:
@@ -824,12 +886,16 @@ void ts_destroy(ts_handle *h)
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    for (auto &g : h->gexec)
-        if (g) cudaGraphExecDestroy(g);
-    for (auto &g : h->graph)
-        if (g) cudaGraphDestroy(g);
+    for (auto &gv : h->gexec)
+        for (auto &g : gv)
+            if (g) cudaGraphExecDestroy(g);
+    for (auto &gv : h->graph)
+        for (auto &g : gv)
+            if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) cudaFree(gr.d);
     cudaFree(h->d_all);
+    cudaFree(h->d_perim);
+    cudaFree(h->d_err_next);
     cudaFree(h->d_rseg);
     cudaFree(h->d_pseg);
     cudaFree(h->d_heta);

@@ -24,7 +24,9 @@ struct DevBlock {
     int32_t has_nman, pad;
 };
 
-// one unit of the march kernels: rows [i0, i1) x output columns [j0, j1)
+// one unit of the march kernels: rows [i0, i1) x output columns [j0, j1);
+// pad = end of the tile's fused-mass columns (interior, not a column-tile
+// boundary); also used as plain cell rectangles by the flat kernels
 struct Tile {
     int32_t blk, i0, i1, j0, j1, pad;
 };
@@ -77,12 +79,15 @@ struct StepArgs {
     int cur;                        // "old" buffer index
     double thr;
     unsigned long long *err;
+    unsigned long long *err_next;   // errors of the fused next-step mass
     const int *acc_flag;            // fold previous step's outputs in K_mass
 };
 
 void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
-void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
+void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fuse,
+                     cudaStream_t s);
+void launch_promote(const StepArgs &a, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, int nseg, int64_t nelem, double *stage,
                      int mode, cudaStream_t s);
 void launch_prolong(const StepArgs &a, const PSeg *segs, int nseg, int64_t nelem, double *stage,
