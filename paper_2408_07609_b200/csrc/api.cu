@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -50,6 +51,7 @@ struct Group {
     int W = 0;
     std::vector<Tile> tiles;
     Tile *d = nullptr;
+    int *d_fix = nullptr;        // failed-guard tile list (exact re-run)
 };
 
 }  // namespace
@@ -70,6 +72,8 @@ struct ts_handle {
     int n_all = 0;
     Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
     int n_perim = 0;
+    int *d_fix_count = nullptr;           // one counter per group
+    bool fuse = false;                    // fused next-step interior mass (see enqueue_step)
     RSeg *d_rseg = nullptr;
     int n_rseg = 0;
     int64_t r_elems = 0;
@@ -163,11 +167,14 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (mark(2)) return TS_ERR_CUDA;
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
     if (mark(3)) return TS_ERR_CUDA;
-    for (auto &gr : h->groups)
-        if (!gr.tiles.empty()) {
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, s);
-            ++n;
-        }
+    CK(cudaMemsetAsync(h->d_fix_count, 0, 4 * sizeof(int), s));
+    for (int k = 0; k < 4; ++k) {
+        Group &gr = h->groups[k];
+        if (gr.tiles.empty()) continue;
+        launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0,
+                        FixList{gr.d_fix, h->d_fix_count + k}, s);
+        n += 2;
+    }
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
     if (mark(5)) return TS_ERR_CUDA;
@@ -210,7 +217,7 @@ int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         if (rc) return rc;
         if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-        if (variant == kFuse) h->launches = nl;
+        if (variant == (h->fuse ? kFuse : kMassAll)) h->launches = nl;
         size_t nn = 0;
         CK(cudaGraphGetNodes(g, nullptr, &nn));
         std::vector<cudaGraphNode_t> nodes(nn);
@@ -461,8 +468,12 @@ int create_impl(const ts_desc *d, ts_handle *h)
             for (int cc : cut_cols) add_rect(b, 1, ni - 1, cc, cc + 1);
         }
     }
-    for (auto &gr : h->groups)
+    for (auto &gr : h->groups) {
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
+        if (!gr.tiles.empty()) CK(cudaMalloc((void **)&gr.d_fix, gr.tiles.size() * sizeof(int)));
+    }
+    CK(cudaMalloc((void **)&h->d_fix_count, 4 * sizeof(int)));
+    CK(cudaMemset(h->d_fix_count, 0, 4 * sizeof(int)));
     {
         std::vector<Tile> all;
         for (auto &gr : h->groups) all.insert(all.end(), gr.tiles.begin(), gr.tiles.end());
@@ -627,8 +638,9 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
     CK(cudaDeviceSynchronize());
+    if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
     cudaGraphExec_t g;
-    return get_graph(h, kFuse, 0, &g);
+    return get_graph(h, h->fuse ? kFuse : kMassAll, 0, &g);
 }
 
 int check_error(ts_handle *h)
@@ -678,6 +690,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
     // others only the perimeter cells the previous (fused) momentum kernel
     // left; every step but the last fuses the next step's interior mass
     auto variant_of = [&](int64_t k) {
+        if (!h->fuse) return (int)kMassAll;
         return (k == 0 ? kMassAll : 0) | (k + 1 < n_steps ? kFuse : 0);
     };
     // the fold flag is cleared for the very first step of the simulation
@@ -786,8 +799,13 @@ int ts_phase(ts_handle *h, int32_t phase)
         break;
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
     case TS_PH_MOMENTUM:
-        for (auto &gr : h->groups)
-            if (!gr.tiles.empty()) launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
+        CK(cudaMemsetAsync(h->d_fix_count, 0, 4 * sizeof(int), s));
+        for (int k = 0; k < 4; ++k) {
+            Group &gr = h->groups[k];
+            if (!gr.tiles.empty())
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false,
+                                FixList{gr.d_fix, h->d_fix_count + k}, s);
+        }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
     case TS_PH_PROLONG:
@@ -892,7 +910,11 @@ void ts_destroy(ts_handle *h)
     for (auto &gv : h->graph)
         for (auto &g : gv)
             if (g) cudaGraphDestroy(g);
-    for (auto &gr : h->groups) cudaFree(gr.d);
+    for (auto &gr : h->groups) {
+        cudaFree(gr.d);
+        cudaFree(gr.d_fix);
+    }
+    cudaFree(h->d_fix_count);
     cudaFree(h->d_all);
     cudaFree(h->d_perim);
     cudaFree(h->d_err_next);
