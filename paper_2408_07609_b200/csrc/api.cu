@@ -51,7 +51,6 @@ struct Group {
     int W = 0;
     std::vector<Tile> tiles;
     Tile *d = nullptr;
-    int *d_fix = nullptr;        // failed-guard tile list (exact re-run)
 };
 
 }  // namespace
@@ -72,7 +71,6 @@ struct ts_handle {
     int n_all = 0;
     Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
     int n_perim = 0;
-    int *d_fix_count = nullptr;           // one counter per group
     bool fuse = false;                    // fused next-step interior mass (see enqueue_step)
     RSeg *d_rseg = nullptr;
     int n_rseg = 0;
@@ -167,13 +165,11 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (mark(2)) return TS_ERR_CUDA;
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
     if (mark(3)) return TS_ERR_CUDA;
-    CK(cudaMemsetAsync(h->d_fix_count, 0, 4 * sizeof(int), s));
     for (int k = 0; k < 4; ++k) {
         Group &gr = h->groups[k];
         if (gr.tiles.empty()) continue;
-        launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0,
-                        FixList{gr.d_fix, h->d_fix_count + k}, s);
-        n += 2;
+        launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, s);
+        ++n;
     }
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
@@ -470,10 +466,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     for (auto &gr : h->groups) {
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
-        if (!gr.tiles.empty()) CK(cudaMalloc((void **)&gr.d_fix, gr.tiles.size() * sizeof(int)));
     }
-    CK(cudaMalloc((void **)&h->d_fix_count, 4 * sizeof(int)));
-    CK(cudaMemset(h->d_fix_count, 0, 4 * sizeof(int)));
     {
         std::vector<Tile> all;
         for (auto &gr : h->groups) all.insert(all.end(), gr.tiles.begin(), gr.tiles.end());
@@ -799,12 +792,10 @@ int ts_phase(ts_handle *h, int32_t phase)
         break;
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
     case TS_PH_MOMENTUM:
-        CK(cudaMemsetAsync(h->d_fix_count, 0, 4 * sizeof(int), s));
         for (int k = 0; k < 4; ++k) {
             Group &gr = h->groups[k];
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false,
-                                FixList{gr.d_fix, h->d_fix_count + k}, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
@@ -912,9 +903,7 @@ void ts_destroy(ts_handle *h)
             if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) {
         cudaFree(gr.d);
-        cudaFree(gr.d_fix);
     }
-    cudaFree(h->d_fix_count);
     cudaFree(h->d_all);
     cudaFree(h->d_perim);
     cudaFree(h->d_err_next);

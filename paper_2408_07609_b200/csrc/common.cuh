@@ -73,12 +73,6 @@ __host__ __device__ __forceinline__ double np_sign(double x)
     return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : (x == 0.0 ? 0.0 : x));
 }
 
-// tiles whose fast-path guards failed, redone by the exact kernel variant
-struct FixList {
-    int *list;
-    int *count;
-};
-
 // ---- launchers (step_kernels.cu) ----
 struct StepArgs {
     const DevBlock *blocks;
@@ -92,7 +86,7 @@ struct StepArgs {
 void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fuse,
-                     const FixList &fix, cudaStream_t s);
+                     cudaStream_t s);
 void launch_promote(const StepArgs &a, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, int nseg, int64_t nelem, double *stage,
                      int mode, cudaStream_t s);
