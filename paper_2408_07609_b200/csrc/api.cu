@@ -61,6 +61,7 @@ struct ts_handle {
     double dt = 0, g = 0, thr = 0;
     int nb = 0;
     std::vector<ts_block_desc> desc;      // pointers not retained
+    std::vector<size_t> off;              // block offset inside its owner's arena
     std::vector<DevBlock> hb;             // host mirror of the device table
     DevBlock *d_blocks = nullptr;
     char *arena = nullptr;
@@ -72,6 +73,13 @@ struct ts_handle {
     Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
     int n_perim = 0;
     bool fuse = false;                    // fused next-step interior mass (see enqueue_step)
+    // multi-GPU (one process per GPU): peer arenas mapped by CUDA IPC
+    unsigned long long *d_sig = nullptr;  // [0, nranks): peers' epochs; [nranks]: own epoch
+    std::vector<char *> peer_arena;
+    std::vector<unsigned long long *> peer_sig;
+    unsigned long long **d_peer_sig = nullptr;
+    int imported = 0;
+    bool x_restrict = false, x_halo = false, x_prolong = false;   // cross-rank traffic per phase
     RSeg *d_rseg = nullptr;
     int n_rseg = 0;
     int64_t r_elems = 0;
@@ -116,10 +124,23 @@ StepArgs args_of(const ts_handle *h, int cur)
     a.err = h->d_err;
     a.err_next = h->d_err_next;
     a.acc_flag = h->d_accflag;
+    a.multi = h->nranks > 1;
     return a;
 }
 
 enum { kMassAll = 1, kFuse = 2 };
+
+void barrier(ts_handle *h, cudaStream_t s)
+{
+    BarrierArgs b;
+    b.peer_flags = h->d_peer_sig;
+    b.my_flags = h->d_sig;
+    b.epoch = h->d_sig + h->nranks;
+    b.err = h->d_err;
+    b.nranks = h->nranks;
+    b.rank = h->rank;
+    launch_barrier(b, s);
+}
 
 // The step body, in the reference's phase order (runner.py:352-365).  When
 // `events` the phase boundaries are recorded (external event nodes when
@@ -152,9 +173,14 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
         if (h->n_perim) { launch_mass(a, h->d_perim, h->n_perim, true, s); ++n; }
     }
     if (mark(1)) return TS_ERR_CUDA;
-    if (h->r_elems) {
+    // multi-GPU phase barriers: only around phases with
+    // cross-rank stores; each one orders this rank's peer stores before the
+    // readers' next phase and keeps writers from overtaking readers
+    if (h->x_restrict) { barrier(h, s); ++n; }
+    if (h->r_elems || h->x_restrict) {
         if (h->r_two_pass) {
             launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
+            if (h->x_restrict) { barrier(h, s); ++n; }
             launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 2, s);
             n += 2;
         } else {
@@ -162,8 +188,10 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
             ++n;
         }
     }
+    if (h->x_restrict) { barrier(h, s); ++n; }
     if (mark(2)) return TS_ERR_CUDA;
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
+    if (h->x_halo) { barrier(h, s); ++n; }
     if (mark(3)) return TS_ERR_CUDA;
     for (int k = 0; k < 4; ++k) {
         Group &gr = h->groups[k];
@@ -174,9 +202,11 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
     if (mark(5)) return TS_ERR_CUDA;
-    if (h->p_elems) {
+    if (h->x_prolong) { barrier(h, s); ++n; }
+    if (h->p_elems || h->x_prolong) {
         if (h->p_two_pass) {
             launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 1, s);
+            if (h->x_prolong) { barrier(h, s); ++n; }
             launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 2, s);
             n += 2;
         } else {
@@ -184,6 +214,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
             ++n;
         }
     }
+    if (h->x_prolong) { barrier(h, s); ++n; }
     if (mark(6)) return TS_ERR_CUDA;
     if (h->n_hflux) { launch_copies(a, h->d_hflux, h->n_hflux, false, s); ++n; }
     // "output" is folded into the next step's K_mass (and the end-of-run
@@ -336,6 +367,23 @@ int upload(Tv **dptr, const std::vector<Tv> &v)
     return TS_OK;
 }
 
+// carve one block's arrays out of an arena region (same order and sizes on
+// every rank; the Manning slot is always reserved so layouts agree without
+// knowing a peer block's Manning representation)
+void place_block(DevBlock &B, char *p, bool with_nman)
+{
+    const size_t P = B.P;
+    const size_t cell = (size_t)(B.ni + 4) * P, mrows = (size_t)(B.ni + 5) * P, acc = (size_t)B.ni * P;
+    auto take = [&](size_t n) { double *q = (double *)p; p += align_up(n * 8, 256); return q; };
+    B.eta[0] = take(cell); B.eta[1] = take(cell);
+    B.m[0] = take(mrows); B.m[1] = take(mrows);
+    B.n[0] = take(cell); B.n[1] = take(cell);
+    B.h = take(cell);
+    double *nm = take(cell);
+    B.nman = with_nman ? nm : nullptr;
+    B.acc_eta = take(acc); B.acc_speed = take(acc); B.acc_inund = take(acc);
+}
+
 int create_impl(const ts_desc *d, ts_handle *h)
 {
     if (!d) return fail(TS_ERR_INVALID, "null descriptor");
@@ -361,25 +409,30 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaEventCreate(&h->t0));
     CK(cudaEventCreate(&h->t1));
 
-    // ---- arena
+    // ---- arena: every rank computes the same per-owner layout for ALL
+    // blocks, so a peer block's arrays are (peer arena base + offset) once
+    // the peer's arena is mapped (ts_ipc_import)
     h->desc.assign(d->blocks, d->blocks + d->n_blocks);
     h->hb.assign(h->nb, DevBlock{});
-    std::vector<size_t> off(h->nb, 0), sizes;
-    size_t total = 0;
+    h->off.assign(h->nb, 0);
+    std::vector<size_t> owner_total(h->nranks, 0);
     for (int b = 0; b < h->nb; ++b) {
         const ts_block_desc &bd = d->blocks[b];
         if (bd.ni < 1 || bd.nj < 1) return fail(TS_ERR_INVALID, "block %lld is %dx%d", (long long)bd.block_id, bd.ni, bd.nj);
-        if (bd.owner != h->rank) continue;
-        if (!bd.h_ext || !bd.eta0) return fail(TS_ERR_INVALID, "block %lld: missing h_ext/eta0", (long long)bd.block_id);
+        if (bd.owner < 0 || bd.owner >= h->nranks)
+            return fail(TS_ERR_INVALID, "block %lld: owner %d outside [0, %d)", (long long)bd.block_id, bd.owner, h->nranks);
+        if (bd.owner == h->rank && (!bd.h_ext || !bd.eta0))
+            return fail(TS_ERR_INVALID, "block %lld: missing h_ext/eta0", (long long)bd.block_id);
         const size_t P = align_up((size_t)bd.nj + 5, 4);
         const size_t cell = (size_t)(bd.ni + 4) * P, mrows = (size_t)(bd.ni + 5) * P, acc = (size_t)bd.ni * P;
         size_t need = 0;
         need += 2 * align_up(cell * 8, 256) + 2 * align_up(mrows * 8, 256) + 2 * align_up(cell * 8, 256);
-        need += align_up(cell * 8, 256) * (bd.nman_ext ? 2 : 1);
+        need += 2 * align_up(cell * 8, 256);         // h and (reserved) Manning n
         need += 3 * align_up(acc * 8, 256);
-        off[b] = total;
-        total += need;
+        h->off[b] = owner_total[bd.owner];
+        owner_total[bd.owner] += need;
     }
+    const size_t total = owner_total[h->rank];
     h->arena_bytes = total;
     if (total) {
         CK(cudaMalloc((void **)&h->arena, total));
@@ -398,16 +451,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
         B.kf = (B.dtg * bd.manning) * bd.manning;
         B.has_nman = bd.nman_ext ? 1 : 0;
         if (bd.owner != h->rank) continue;
+        place_block(B, h->arena + h->off[b], B.has_nman != 0);
         const size_t P = B.P;
-        const size_t cell = (size_t)(bd.ni + 4) * P, mrows = (size_t)(bd.ni + 5) * P, acc = (size_t)bd.ni * P;
-        char *p = h->arena + off[b];
-        auto take = [&](size_t n) { double *q = (double *)p; p += align_up(n * 8, 256); return q; };
-        B.eta[0] = take(cell); B.eta[1] = take(cell);
-        B.m[0] = take(mrows); B.m[1] = take(mrows);
-        B.n[0] = take(cell); B.n[1] = take(cell);
-        B.h = take(cell);
-        B.nman = bd.nman_ext ? take(cell) : nullptr;
-        B.acc_eta = take(acc); B.acc_speed = take(acc); B.acc_inund = take(acc);
         // h_ext / n_ext with ghosts (kernels.py:53-62, exchange.py:281-300)
         CK(cudaMemcpy2D(B.h, P * 8, bd.h_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
                         bd.ni + 4, cudaMemcpyHostToDevice));
@@ -493,11 +538,14 @@ int create_impl(const ts_desc *d, ts_handle *h)
             const int count = s.parent_hi - s.parent_lo;
             if (count < 0 || s.child_hi - s.child_lo != 3 * count)
                 return fail(TS_ERR_INVALID, "restriction segment %d: spans disagree", k);
-            if (!owned(s.child) || count == 0) continue;
+            if (count == 0) continue;
             const bool ns = s.side >= TS_SOUTH;
-            segs.push_back(RSeg{s.child, s.parent, ns, s.child_lo, s.ring_start, s.parent_line,
-                                s.parent_lo, count, first});
-            first += count;
+            if (d->blocks[s.child].owner != d->blocks[s.parent].owner) h->x_restrict = true;
+            if (owned(s.child)) {
+                segs.push_back(RSeg{s.child, s.parent, ns, s.child_lo, s.ring_start, s.parent_line,
+                                    s.parent_lo, count, first});
+                first += count;
+            }
             for (int p = 0; p < count; ++p) {
                 written.insert(key(s.parent, ns ? s.parent_lo + p : s.parent_line, ns ? s.parent_line : s.parent_lo + p));
                 for (int u = 0; u < 3; ++u)
@@ -530,11 +578,14 @@ int create_impl(const ts_desc *d, ts_handle *h)
             const int count = s.parent_hi - s.parent_lo;
             if (count < 0 || s.child_hi - s.child_lo != 3 * count)
                 return fail(TS_ERR_INVALID, "prolongation segment %d: spans disagree", k);
-            if (!owned(s.parent) || count == 0) continue;
+            if (count == 0) continue;
             const bool ns = s.side >= TS_SOUTH;
-            segs.push_back(PSeg{s.parent, s.child, ns, s.child_lo, s.child_face_line, s.parent_face_line,
-                                s.parent_lo, count, first});
-            first += 3 * count;
+            if (d->blocks[s.child].owner != d->blocks[s.parent].owner) h->x_prolong = true;
+            if (owned(s.parent)) {
+                segs.push_back(PSeg{s.parent, s.child, ns, s.child_lo, s.child_face_line, s.parent_face_line,
+                                    s.parent_lo, count, first});
+                first += 3 * count;
+            }
             const int arr = ns ? 2 : 1;
             for (int p = 0; p < count; ++p) {
                 read.insert(key(s.parent, arr, ns ? s.parent_lo + p : s.parent_face_line,
@@ -565,6 +616,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
             if (span < 0 || e.recv_hi - e.recv_lo != span)
                 return fail(TS_ERR_INVALID, "halo entry %d: spans disagree", k);
             const ts_block_desc &S = d->blocks[e.sender], &R = d->blocks[e.receiver];
+            if (S.owner != R.owner) h->x_halo = true;
             const int Ps = h->hb[e.sender].P, Pr = h->hb[e.receiver].P;
             const int rside = kOpp[e.side];
             for (int l = 0; l < 2; ++l)
@@ -632,6 +684,17 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     CK(cudaDeviceSynchronize());
     if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
+    if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
+    // signal area: peers' epochs + own epoch; its IPC handle is exported
+    CK(cudaMalloc((void **)&h->d_sig, (h->nranks + 1) * sizeof(unsigned long long)));
+    CK(cudaMemset(h->d_sig, 0, (h->nranks + 1) * sizeof(unsigned long long)));
+    h->peer_arena.assign(h->nranks, nullptr);
+    h->peer_sig.assign(h->nranks, nullptr);
+    h->peer_arena[h->rank] = h->arena;
+    h->peer_sig[h->rank] = h->d_sig;
+    CK(cudaMalloc((void **)&h->d_peer_sig, h->nranks * sizeof(unsigned long long *)));
+    CK(cudaMemcpy(h->d_peer_sig, h->peer_sig.data(), h->nranks * sizeof(unsigned long long *),
+                  cudaMemcpyHostToDevice));
     cudaGraphExec_t g;
     return get_graph(h, h->fuse ? kFuse : kMassAll, 0, &g);
 }
@@ -643,6 +706,8 @@ int check_error(ts_handle *h)
     if (key == TS_NO_ERROR) return TS_OK;
     const int order = (int)(key >> 50), what = (int)((key >> 48) & 3);
     const long long i = (long long)((key >> 24) & 0xffffff) - 4, j = (long long)(key & 0xffffff) - 4;
+    if (what == 3)
+        return fail(TS_ERR_CUDA, "rank %d: peer rank %lld did not reach a phase barrier within 30 s", h->rank, i);
     static const char *names[3] = {"water level", "x-flux", "y-flux"};
     return fail(TS_ERR_NUMERICS, "non-finite %s in block %lld at local cell (%lld, %lld)", names[what],
                 (long long)h->desc[order].block_id, i, j);
@@ -678,6 +743,9 @@ int ts_run(ts_handle *h, int64_t n_steps)
     CK(cudaSetDevice(h->device));
     if (int rc = check_error(h)) return rc;
     if (n_steps == 0) return TS_OK;
+    if (h->imported != h->nranks - 1)
+        return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
+                    h->rank, h->imported, h->nranks - 1);
     cudaStream_t s = h->stream;
     // step k of this call: the first runs the full continuity pass, the
     // others only the perimeter cells the previous (fused) momentum kernel
@@ -916,6 +984,13 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_err);
     cudaFree(h->d_accflag);
     cudaFree(h->d_blocks);
+    for (int p = 0; p < (int)h->peer_arena.size(); ++p)
+        if (p != h->rank) {
+            if (h->peer_arena[p]) cudaIpcCloseMemHandle(h->peer_arena[p]);
+            if (h->peer_sig[p]) cudaIpcCloseMemHandle(h->peer_sig[p]);
+        }
+    cudaFree(h->d_sig);
+    cudaFree(h->d_peer_sig);
     cudaFree(h->arena);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -928,14 +1003,45 @@ void ts_destroy(ts_handle *h)
 
 int ts_ipc_export(ts_handle *h, void *out, int64_t len)
 {
-    (void)h; (void)out; (void)len;
-    return fail(TS_ERR_INVALID, "multi-GPU exchange not built into this library version");
+    if (!h || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (len < (int64_t)(2 * sizeof(cudaIpcMemHandle_t) + 8)) return fail(TS_ERR_INVALID, "IPC blob too short");
+    CK(cudaSetDevice(h->device));
+    char *o = (char *)out;
+    std::memset(o, 0, (size_t)len);
+    if (h->arena) CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)o, h->arena));
+    CK(cudaIpcGetMemHandle((cudaIpcMemHandle_t *)(o + sizeof(cudaIpcMemHandle_t)), h->d_sig));
+    const int64_t bytes = (int64_t)h->arena_bytes;
+    std::memcpy(o + 2 * sizeof(cudaIpcMemHandle_t), &bytes, 8);
+    return TS_OK;
 }
 
-int ts_ipc_import(ts_handle *h, int32_t peer_rank, const void *in, int64_t len)
+int ts_ipc_import(ts_handle *h, int32_t peer, const void *in, int64_t len)
 {
-    (void)h; (void)peer_rank; (void)in; (void)len;
-    return fail(TS_ERR_INVALID, "multi-GPU exchange not built into this library version");
+    if (!h || !in) return fail(TS_ERR_INVALID, "null argument");
+    if (peer < 0 || peer >= h->nranks || peer == h->rank) return fail(TS_ERR_INVALID, "bad peer rank %d", peer);
+    if (len < (int64_t)(2 * sizeof(cudaIpcMemHandle_t) + 8)) return fail(TS_ERR_INVALID, "IPC blob too short");
+    CK(cudaSetDevice(h->device));
+    const char *b = (const char *)in;
+    int64_t bytes = 0;
+    std::memcpy(&bytes, b + 2 * sizeof(cudaIpcMemHandle_t), 8);
+    void *arena = nullptr, *sig = nullptr;
+    if (bytes > 0) {
+        cudaIpcMemHandle_t ha;
+        std::memcpy(&ha, b, sizeof ha);
+        CK(cudaIpcOpenMemHandle(&arena, ha, cudaIpcMemLazyEnablePeerAccess));
+    }
+    cudaIpcMemHandle_t hs;
+    std::memcpy(&hs, b + sizeof(cudaIpcMemHandle_t), sizeof hs);
+    CK(cudaIpcOpenMemHandle(&sig, hs, cudaIpcMemLazyEnablePeerAccess));
+    h->peer_arena[peer] = (char *)arena;
+    h->peer_sig[peer] = (unsigned long long *)sig;
+    for (int k = 0; k < h->nb; ++k)
+        if (h->desc[k].owner == peer) place_block(h->hb[k], (char *)arena + h->off[k], false);
+    CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_peer_sig, h->peer_sig.data(), h->nranks * sizeof(unsigned long long *),
+                  cudaMemcpyHostToDevice));
+    h->imported += 1;
+    return TS_OK;
 }
 
 void ts_cbrt_host(const double *in, double *out, int64_t n)

@@ -81,7 +81,20 @@ struct StepArgs {
     unsigned long long *err;
     unsigned long long *err_next;   // errors of the fused next-step mass
     const int *acc_flag;            // fold previous step's outputs in K_mass
+    int multi;                      // >1 rank: exchange kernels fence their peer stores
 };
+
+// inter-GPU phase barrier (one process per GPU): every rank bumps its epoch,
+// stores it into each peer's flag slot over NVLink and spins until every
+// peer's epoch reached its own (timeout -> error key what = 3)
+struct BarrierArgs {
+    unsigned long long *const *peer_flags;   // [n_ranks] peer flag arrays (own at [rank])
+    unsigned long long *my_flags;            // this rank's flag array, slot per peer
+    unsigned long long *epoch;
+    unsigned long long *err;
+    int nranks, rank;
+};
+void launch_barrier(const BarrierArgs &b, cudaStream_t s);
 
 void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);

@@ -237,13 +237,28 @@ class Simulation:
     reference.  In a single process all blocks live on ``device``.
     """
 
-    def __init__(self, system, settings, plan=None, *, device: int = 0, tile_rows: int = 0):
+    def __init__(self, system, settings, plan=None, *, device: int | None = None, tile_rows: int = 0,
+                 distributed: bool | None = None, group=None):
+        from . import distributed as D
         ordered = system.all_blocks()
+        rank, world, local = D.dist_context(group)
+        if distributed is None:
+            distributed = world > 1
+        if not distributed:
+            rank, world = 0, 1
         if plan is None:
-            from .balance import equal_cell_plan
-            plan = equal_cell_plan([b.ni * b.nj for _, b in ordered], 1)
+            from .balance import equal_cell_plan, minmax_plan
+            cells = [b.ni * b.nj for _, b in ordered]
+            plan = equal_cell_plan(cells, 1) if world == 1 else minmax_plan(cells, world)
         if plan.n_blocks != len(ordered):
             raise ValueError(f"plan covers {plan.n_blocks} blocks, system has {len(ordered)}")
+        # one process per GPU: plan rank r is GPU r; a single process runs
+        # every rank's blocks on its one GPU (the plan then fixes only the
+        # exchange apply order and the per-rank report, as in the reference)
+        self.rank, self.world, self.group = rank, world, group
+        self.owner = D.owners_from_plan(system, plan, world) if world > 1 else [0] * len(ordered)
+        if device is None:
+            device = local if world > 1 else 0
         self.system, self.settings, self.plan = system, settings, plan
         self.rank_of = {b.block_id: plan.rank_of(k) for k, (_, b) in enumerate(ordered)}
         self.n_ranks = plan.n_ranks
@@ -258,11 +273,12 @@ class Simulation:
             self.contexts[plan.rank_of(k)].block_ids.append(b.block_id)
         self._h = None
         self._create(ordered, tile_rows)
+        if world > 1:
+            D.exchange_peer_handles(self._ipc_export, self._ipc_import, rank, world, group)
         thr = settings.wet_threshold
-        self.states = {b.block_id: DeviceBlockState(self, self.index[b.block_id], b, thr)
-                       for _, b in ordered}
-        self.accumulators = {b.block_id: DeviceAccumulators(self, self.index[b.block_id], b)
-                             for _, b in ordered}
+        mine = [(k, b) for k, (_, b) in enumerate(ordered) if self.owner[k] == rank]
+        self.states = {b.block_id: DeviceBlockState(self, k, b, thr) for k, b in mine}
+        self.accumulators = {b.block_id: DeviceAccumulators(self, k, b) for k, b in mine}
         self.steps_done = 0
         self._wet_role = "new"
 
@@ -276,7 +292,7 @@ class Simulation:
             h, nman, eta0 = arrays[b.block_id]
             keep += [h, nman, eta0]
             d = blocks[k]
-            d.block_id, d.ni, d.nj, d.owner = b.block_id, b.ni, b.nj, 0
+            d.block_id, d.ni, d.nj, d.owner = b.block_id, b.ni, b.nj, self.owner[k]
             d.level = self.system.levels.index(lvl)
             d.dx = lvl.dx
             d.manning = float(b.manning_n) if nman is None else 0.0
@@ -306,12 +322,21 @@ class Simulation:
             arrs.append(arr)
             setattr(desc, name, arr)
         desc.n_halo, desc.n_restrict, desc.n_prolong, desc.n_edges = len(halo), len(rseg), len(pseg), len(edges)
-        desc.rank, desc.n_ranks, desc.device, desc.tile_rows = 0, 1, self.device, tile_rows
+        desc.rank, desc.n_ranks, desc.device, desc.tile_rows = self.rank, self.world, self.device, tile_rows
         hptr = ctypes.c_void_p()
         N.check(L.ts_create(ctypes.byref(desc), ctypes.byref(hptr)))
         self._h = hptr
         self._descr_counts = dict(halo=len(halo), restrict=len(rseg), prolong=len(pseg), edges=len(edges))
         del keep, arrs
+
+    def _ipc_export(self) -> bytes:
+        buf = (ctypes.c_char * 256)()
+        N.check(N.lib().ts_ipc_export(self._h, buf, 256))
+        return bytes(buf)
+
+    def _ipc_import(self, peer: int, blob: bytes):
+        buf = (ctypes.c_char * len(blob)).from_buffer_copy(blob)
+        N.check(N.lib().ts_ipc_import(self._h, peer, buf, len(blob)))
 
     def close(self):
         if self._h is not None:
@@ -351,9 +376,37 @@ class Simulation:
         self._invalidate()
         if n:
             self._wet_role = "old"
+        if self.world > 1:
+            self._distributed_status(rc, threaded)
+            return
         if rc == N.TS_ERR_NUMERICS:
             self._raise_numerics(threaded)
         N.check(rc)
+
+    def _distributed_status(self, rc, threaded):
+        """Agree on the first failure over ranks (the reference's serial
+        order: lowest block, x before y flux, C order) and raise it on all."""
+        from . import distributed as D
+        local = None
+        if rc == N.TS_ERR_NUMERICS:
+            blk, what = ctypes.c_int32(-1), ctypes.c_int32(0)
+            i, j = ctypes.c_int64(0), ctypes.c_int64(0)
+            N.lib().ts_error_info(self._h, ctypes.byref(blk), ctypes.byref(what), ctypes.byref(i),
+                                  ctypes.byref(j))
+            local = (blk.value, what.value, i.value, j.value)
+        elif rc != N.TS_OK:
+            local = (-1, 9, 0, 0, N.lib().ts_last_error().decode())
+        first = D.first_error(local, self.group)
+        if first is None:
+            return
+        if first[0] < 0:
+            raise N.NativeError(N.TS_ERR_CUDA, first[4])
+        bid = self.system.all_blocks()[first[0]][1].block_id
+        what = ("water level", "x-flux", "y-flux")[first[1]]
+        msg = f"non-finite {what} in block {bid} at local cell ({first[2]}, {first[3]})"
+        if threaded and self.n_ranks > 1:
+            raise SimulationAborted(f"rank {self.rank_of.get(bid, 0)} failed: {msg}") from NumericsError(msg)
+        raise NumericsError(msg)
 
     def run(self, n_steps: int, threaded: bool = True, timeout: float = 60.0,
             trace_path: str | None = None, record_phases: bool = False, on_step=None) -> RunReport:
