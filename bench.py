@@ -134,8 +134,8 @@ def profiled_traffic():
     p = os.path.join(ROOT, "profiles", "momentum_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f)
-    except (OSError, ValueError):
+            return float(json.load(f)["bytes_per_step"])
+    except (OSError, ValueError, KeyError):
         return None
 
 
@@ -178,73 +178,97 @@ def run_ours(args):
     rank, world, local = dist_env()
     import torch
     import paper_2408_07609_b200 as P
+    from paper_2408_07609_b200 import distributed as D
+    from paper_2408_07609_b200.runner import host_block_arrays
+    torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
     system, settings, label = build_workload(P, args.config, args.scale)
     cells = system.cell_count
-    if world > 1:
-        raise SystemExit("multi-GPU decomposition: see DESIGN.md §7 (not in this build)")
-    sim = P.Simulation(system, settings, device=local)
+    counts = [b.cell_count for _, b in system.all_blocks()]
+    # blocks -> GPUs: exact min-max partition of the level-ordered block list
+    plan = P.minmax_plan(counts, world) if world > 1 else P.equal_cell_plan(counts, 1)
+    sim = P.Simulation(system, settings, plan, device=local, distributed=world > 1)
     ext = torch.cuda.ExternalStream(sim.stream_ptr, device=local)
     sim.run(args.warmup, threaded=False)
     sim.set_timing(True)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         start.record(ext)
         sim.run(args.steps, threaded=False)
         end.record(ext)
         torch.cuda.synchronize()
+    barrier()
     sim.set_timing(False)
-    t = start.elapsed_time(end) / 1e3
+    t_local = start.elapsed_time(end) / 1e3
+    t = D.max_over_ranks(t_local) if world > 1 else t_local
     mass_s, mom_s, step_s = sim.kernel_seconds()
     launches = sim.launches_per_step * args.steps + 4
 
-    # end to end through the public API with host buffers
-    arrays = __import__("paper_2408_07609_b200.runner", fromlist=["x"]).host_block_arrays(system, settings)
+    # end to end through the public API with host buffers: upload the host
+    # inputs, K steps, download the result maps (every rank its own blocks)
+    arrays = host_block_arrays(system, settings)
+    barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h2d = sim.upload_initial_state(arrays)
     sim.run(args.steps, threaded=False)
     _, d2h = sim.download_outputs()
-    te = time.perf_counter() - t0
+    te_local = time.perf_counter() - t0
+    te = D.max_over_ranks(te_local) if world > 1 else te_local
+    if world > 1:
+        h2d = sum(D.all_gather_bytes(h2d))
+        d2h = sum(D.all_gather_bytes(d2h))
 
     peak, peak_src = measured_peaks()
-    achieved = ALG_BYTES_MOM * cells / mom_s / 1e9 if mom_s > 0 else None
+    my_cells = sum(c for k, c in enumerate(counts) if sim.owner[k] == rank)
+    achieved = ALG_BYTES_MOM * my_cells / mom_s / 1e9 if mom_s > 0 else None
     traffic = profiled_traffic()
     line = {
         "metric": "Gcell-updates/s", "value": cells * args.steps / t / 1e9, "unit": "Gcell/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cells": cells, "levels": len(system.levels),
                    "blocks": system.n_blocks, "dt_s": settings.dt,
-                   "parallelism": f"blocks over {world} GPU(s)",
+                   "parallelism": f"blocks over {world} GPU(s) (min-max plan {list(plan.separators)})",
                    "l2": "state 3.8 GB >> 126 MB L2; no flush"},
         "six_hour_wall_s": t / args.steps * SIX_HOURS_STEPS,
         "step_roofline": {"bytes_per_cell_step": ALG_BYTES_STEP,
                           "achieved_gbs": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9,
-                          "frac": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9 / peak},
+                          "frac": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9 / (peak * world)},
         "roofline": {"kernel": "k_momentum", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak if achieved else None,
-                     "traffic": traffic, "alg_bytes_per_launch": ALG_BYTES_MOM * cells,
+                     "traffic": traffic, "alg_bytes_per_launch": ALG_BYTES_MOM * my_cells,
                      "avg_launch_s": mom_s, "peak_source": peak_src,
-                     "mass_kernel_s": mass_s, "step_s_events": step_s},
+                     "mass_kernel_s": mass_s, "step_s_events": step_s, "rank": rank},
         "e2e": {"value": cells * args.steps / te / 1e9, "unit": "Gcell/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "wall_s": te},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu and world == 1:
         rate, threads, dt = cpu_sample(system, settings, steps=1, warm=1)
         line["cpu_baseline"] = {"value": rate, "unit": "Gcell/s", "cores": threads, "kind": "port",
                                 "sample": "1 step of the full workload after 1 warm-up step "
                                           f"({dt:.1f} s)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    sim.close()
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def main():
