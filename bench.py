@@ -232,7 +232,7 @@ def run_ours(args):
     peak, peak_src = measured_peaks()
     my_cells = sum(c for k, c in enumerate(counts) if sim.owner[k] == rank)
     achieved = ALG_BYTES_MOM * my_cells / mom_s / 1e9 if mom_s > 0 else None
-    traffic = profiled_traffic()
+    traffic = profiled_traffic() if world == 1 else None   # the capture is of the 1-GPU step
     line = {
         "metric": "Gcell-updates/s", "value": cells * args.steps / t / 1e9, "unit": "Gcell/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
