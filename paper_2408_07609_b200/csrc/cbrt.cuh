@@ -57,11 +57,14 @@ static const double ts_cbrt_k_host[12] = {TS_CBRT_TABLE};
 TS_HD double ts_cbrt_pos_normal(double x, int extra_exp)
 {
     const uint64_t b = ts_bits(x);
-    const int e = (int)(b >> 52) - 1023;
-    const double m = ts_from_bits((b & 0x000fffffffffffffULL) | 0x3ff0000000000000ULL);
-    const int q = (e >= 0) ? e / 3 : -((2 - e) / 3);
-    const int r = e - 3 * q;
-    const double t = TS_MUL(m, (double)(1 << r));
+    // e = 3q + r with q = floor(e / 3): k = e + 1200 >= 0 and floor(k / 3)
+    // = (k * 21846) >> 16 for k < 32768 (integer ops only, no branch)
+    const int k = (int)(b >> 52) - 1023 + 1200;
+    const int qk = (k * 21846) >> 16;
+    const int q = qk - 400, r = k - 3 * qk;
+    const uint64_t mant = b & 0x000fffffffffffffULL;
+    const double m = ts_from_bits(mant | 0x3ff0000000000000ULL);
+    const double t = ts_from_bits(mant | ((uint64_t)(1023 + r) << 52));     // m * 2^r, exact
     double p = TS_CBRT_K(0);
     p = TS_FMA(p, m, TS_CBRT_K(1));
     p = TS_FMA(p, m, TS_CBRT_K(2));
