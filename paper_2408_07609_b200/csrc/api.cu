@@ -66,13 +66,18 @@ struct ts_handle {
     DevBlock *d_blocks = nullptr;
     char *arena = nullptr;
     size_t arena_bytes = 0;
-    int T = 34;                           // rows per tile; T + 2 must be a multiple of 3
+    int T = 64;                           // rows per march tile; T + 2 must be a multiple of 3
     Group groups[4];                      // W = 1..4 (momentum march)
     Tile *d_all = nullptr;                // every tile (flat mass / fold kernels)
     int n_all = 0;
     Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
     int n_perim = 0;
     bool fuse = false;                    // fused next-step interior mass (see enqueue_step)
+    // the momentum launches of the column-width groups run as parallel
+    // graph branches (the small groups fill the big one's tail)
+    bool mom_par = true;
+    cudaStream_t side[3] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[3] = {};
     // multi-GPU (one process per GPU): peer arenas mapped by CUDA IPC
     unsigned long long *d_sig = nullptr;  // [0, nranks): peers' epochs; [nranks]: own epoch
     std::vector<char *> peer_arena;
@@ -193,11 +198,32 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
     if (h->x_halo) { barrier(h, s); ++n; }
     if (mark(3)) return TS_ERR_CUDA;
-    for (int k = 0; k < 4; ++k) {
-        Group &gr = h->groups[k];
-        if (gr.tiles.empty()) continue;
-        launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, s);
-        ++n;
+    {
+        // largest group on the main stream, the others forked onto side
+        // streams (parallel branches of the captured graph) and joined back
+        int order[4], ng = 0;
+        for (int k = 0; k < 4; ++k)
+            if (!h->groups[k].tiles.empty()) order[ng++] = k;
+        for (int x = 1; x < ng; ++x)
+            for (int y = x; y > 0 && h->groups[order[y]].tiles.size() * h->groups[order[y]].W >
+                                         h->groups[order[y - 1]].tiles.size() * h->groups[order[y - 1]].W; --y)
+                std::swap(order[y], order[y - 1]);
+        const bool par = h->mom_par && ng > 1;
+        if (par) CK(cudaEventRecord(h->ev_fork, s));
+        for (int x = 0; x < ng; ++x) {
+            Group &gr = h->groups[order[x]];
+            cudaStream_t st = s;
+            if (par && x > 0) {
+                st = h->side[x - 1];
+                CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
+            }
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, st);
+            ++n;
+            if (par && x > 0) {
+                CK(cudaEventRecord(h->ev_join[x - 1], st));
+                CK(cudaStreamWaitEvent(s, h->ev_join[x - 1], 0));
+            }
+        }
     }
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
@@ -405,6 +431,9 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     CK(cudaSetDevice(h->device));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    for (auto &st : h->side) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+    for (auto &e : h->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : h->ev) CK(cudaEventCreate(&e));
     CK(cudaEventCreate(&h->t0));
     CK(cudaEventCreate(&h->t1));
@@ -513,8 +542,20 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
     }
     {
+        // cell tiles of the flat kernels (mass + fold, flush): about
+        // mass_cells cells each, whole rows up to 1024 columns
+        int target = 8192;
+        if (const char *f = getenv("TSUNAMI_B200_MASS_CELLS")) target = std::max(256, atoi(f));
         std::vector<Tile> all;
-        for (auto &gr : h->groups) all.insert(all.end(), gr.tiles.begin(), gr.tiles.end());
+        for (int b = 0; b < h->nb; ++b) {
+            if (d->blocks[b].owner != h->rank) continue;
+            const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
+            const int cw = std::min(nj, 1024);
+            const int R = std::max(1, target / cw);
+            for (int j0 = 0; j0 < nj; j0 += cw)
+                for (int i0 = 0; i0 < ni; i0 += R)
+                    all.push_back(Tile{b, i0, std::min(i0 + R, ni), j0, std::min(j0 + cw, nj), 0});
+        }
         h->n_all = (int)all.size();
         if (int rc = upload(&h->d_all, all)) return rc;
         h->n_perim = (int)perim.size();
@@ -685,6 +726,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaDeviceSynchronize());
     if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
     if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
+    if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
     // signal area: peers' epochs + own epoch; its IPC handle is exported
     CK(cudaMalloc((void **)&h->d_sig, (h->nranks + 1) * sizeof(unsigned long long)));
     CK(cudaMemset(h->d_sig, 0, (h->nranks + 1) * sizeof(unsigned long long)));
@@ -997,6 +1039,11 @@ void ts_destroy(ts_handle *h)
     for (auto &e : h->pool) cudaEventDestroy(e);
     if (h->t0) cudaEventDestroy(h->t0);
     if (h->t1) cudaEventDestroy(h->t1);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    for (auto &e : h->ev_join)
+        if (e) cudaEventDestroy(e);
+    for (auto &st : h->side)
+        if (st) cudaStreamDestroy(st);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
