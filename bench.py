@@ -14,7 +14,8 @@ halo-eta, momentum with edge rules, prolongation, halo-flux, output maxima.
   synchronize on both sides, max over ranks); inputs are device resident
   and 3.8 GB > 126 MB L2, so no flush is needed.
 * ``e2e``: the same K steps through the public API with host buffers:
-  upload of the host inputs, K steps, download of the result maps.
+  upload of the page-locked host inputs (bathymetry with ghosts, initial
+  level), K steps, download of the result maps into page-locked buffers.
 * ``roofline``: the momentum kernel (the dominant one), algorithmic bytes
   per launch / its average duration over the timed steps (per-step CUDA
   events inside the graph, on the launch stream), against the measured HBM
@@ -216,13 +217,14 @@ def run_ours(args):
 
     # end to end through the public API with host buffers: upload the host
     # inputs, K steps, download the result maps (every rank its own blocks)
-    arrays = host_block_arrays(system, settings)
+    arrays = host_block_arrays(system, settings, pinned=True)     # page-locked inputs
+    outs = sim.output_buffers(pinned=True)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     h2d = sim.upload_initial_state(arrays)
     sim.run(args.steps, threaded=False)
-    _, d2h = sim.download_outputs()
+    _, d2h = sim.download_outputs(outs)
     te_local = time.perf_counter() - t0
     te = D.max_over_ranks(te_local) if world > 1 else te_local
     if world > 1:

@@ -150,6 +150,9 @@ int ts_phase(ts_handle *h, int32_t phase);
 /* BlockState / OutputAccumulators array access in the reference layout */
 int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_t len);
 int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, int64_t len);
+/* BlockState.set_initial_eta (kernels.py:97-101): the ni*nj interior
+ * initial level into both water-level buffers */
+int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t len);
 /* the first non-finite value of the failing step (kernels.py:115-120):
  * what = 0 water level, 1 x-flux, 2 y-flux; (i, j) local cell */
 int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j);
@@ -177,6 +180,11 @@ void ts_destroy(ts_handle *h);
  * handles, then map every peer's before the first ts_run */
 int ts_ipc_export(ts_handle *h, void *out, int64_t len);
 int ts_ipc_import(ts_handle *h, int32_t peer_rank, const void *in, int64_t len);
+
+/* page-locked host buffers (staging of the host<->device copies of the
+ * public API at full PCIe rate); NULL on failure */
+void *ts_host_alloc(int64_t bytes);
+void ts_host_free(void *p);
 
 /* the friction cube root (kernels.py:240-241 np.cbrt): host twin and device */
 void ts_cbrt_host(const double *in, double *out, int64_t n);

@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 import numpy as np
 
@@ -89,6 +90,11 @@ def lib():
     L.ts_phase.argtypes = [c_void_p, c_int32]
     L.ts_get_field.argtypes = [c_void_p, c_int32, c_int32, c_void_p, c_int64]
     L.ts_set_field.argtypes = [c_void_p, c_int32, c_int32, c_void_p, c_int64]
+    L.ts_set_initial_eta.argtypes = [c_void_p, c_int32, c_void_p, c_int64]
+    L.ts_host_alloc.argtypes = [c_int64]
+    L.ts_host_alloc.restype = c_void_p
+    L.ts_host_free.argtypes = [c_void_p]
+    L.ts_host_free.restype = None
     L.ts_error_info.argtypes = [c_void_p] + [c_void_p] * 4
     L.ts_timings.argtypes = [c_void_p, c_void_p, c_void_p]
     L.ts_steps_done.argtypes = [c_void_p]
@@ -116,7 +122,21 @@ def lib():
 EXPORTED = ("ts_last_error", "ts_abi_version", "ts_create", "ts_run", "ts_phase", "ts_get_field",
             "ts_set_field", "ts_error_info", "ts_timings", "ts_steps_done", "ts_device_bytes",
             "ts_launches_per_step", "ts_set_timing", "ts_kernel_seconds", "ts_stream", "ts_destroy",
-            "ts_ipc_export", "ts_ipc_import", "ts_cbrt_host", "ts_cbrt_device")
+            "ts_ipc_export", "ts_ipc_import", "ts_cbrt_host", "ts_cbrt_device", "ts_set_initial_eta",
+            "ts_host_alloc", "ts_host_free")
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """A float64 array in page-locked host memory (ts_host_alloc), freed when
+    the array is garbage collected."""
+    n = int(np.prod(shape))
+    p = lib().ts_host_alloc(max(1, n) * 8)
+    if not p:
+        raise MemoryError(f"ts_host_alloc of {n * 8} bytes failed")
+    buf = (ctypes.c_double * max(1, n)).from_address(p)
+    arr = np.frombuffer(buf, dtype=np.float64, count=n).reshape(shape)
+    weakref.finalize(buf, lib().ts_host_free, p)
+    return arr
 
 
 def check(rc: int):

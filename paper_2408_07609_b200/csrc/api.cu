@@ -955,6 +955,33 @@ int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, i
     return TS_OK;
 }
 
+int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t len)
+{
+    if (!h || !eta0) return fail(TS_ERR_INVALID, "null argument");
+    FieldGeom g;
+    if (int rc = field_geom(h, block, TS_ETA_OLD, &g)) return rc;
+    const DevBlock &B = h->hb[block];
+    if (len != (int64_t)B.ni * B.nj) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, B.ni, B.nj);
+    CK(cudaSetDevice(h->device));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int k = 0; k < 2; ++k)
+        CK(cudaMemcpy2D(B.eta[k] + 2 * (size_t)B.P + 2, (size_t)B.P * 8, eta0, (size_t)B.nj * 8,
+                        (size_t)B.nj * 8, B.ni, cudaMemcpyHostToDevice));
+    return TS_OK;
+}
+
+void *ts_host_alloc(int64_t bytes)
+{
+    void *p = nullptr;
+    if (bytes <= 0 || cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    return p;
+}
+
+void ts_host_free(void *p)
+{
+    if (p) cudaFreeHost(p);
+}
+
 int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j)
 {
     if (!h) return fail(TS_ERR_INVALID, "null handle");

@@ -98,10 +98,11 @@ def _strip(ni, nj, side, span, sending, g=HALO_WIDTH):
     return slice(g + lo, g + hi), ys
 
 
-def host_block_arrays(system, settings):
+def host_block_arrays(system, settings, pinned: bool = False):
     """Per block id: ghosted h_ext, optional n_ext, interior eta0 — the
     reference's BlockState setup (kernels.py:39-62, 97-101), initial
-    sampling (runner.py:75-80) and fill_bathymetry_halos (exchange.py:281-300)."""
+    sampling (runner.py:75-80) and fill_bathymetry_halos (exchange.py:281-300).
+    ``pinned``: h_ext and eta0 in page-locked memory (ts_host_alloc)."""
     g = HALO_WIDTH
     out = {}
     for lvl in system.levels:
@@ -120,6 +121,12 @@ def host_block_arrays(system, settings):
             eta0 = np.ascontiguousarray(np.broadcast_to(
                 settings.initial.eta0(x[:, None], y[None, :]), (b.ni, b.nj)), dtype=float)
             out[b.block_id] = (h, nman, eta0)
+    if pinned:
+        for bid, (h, nman, eta0) in out.items():
+            hp, ep = N.pinned_empty(h.shape), N.pinned_empty(eta0.shape)
+            hp[...] = h
+            ep[...] = eta0
+            out[bid] = (hp, nman, ep)
     for lvl in system.levels:
         starts = {b.block_id: lattice_origin(b, lvl.dx) for b in lvl.blocks}
         dims = {b.block_id: (b.ni, b.nj) for b in lvl.blocks}
@@ -500,34 +507,44 @@ class Simulation:
         return int(p.value or 0)
 
     def upload_initial_state(self, arrays=None):
-        """Copy the host inputs (ghosted bathymetry, initial level) into the
-        device state again — the host->device leg of an end-to-end run.
-        Returns the bytes copied."""
+        """Copy the host inputs (ghosted bathymetry, initial level) of the
+        owned blocks into the device state again — the host->device leg of an
+        end-to-end run (BlockState construction + set_initial_eta,
+        kernels.py:39-62, 97-101).  ``arrays`` as returned by
+        ``host_block_arrays`` (page-locked with ``pinned=True``).  Returns the
+        bytes copied."""
         if arrays is None:
             arrays = host_block_arrays(self.system, self.settings)
-        nbytes = 0
+        L, nbytes = N.lib(), 0
         for bid, st in self.states.items():
             h, _, eta0 = arrays[bid]
             st._invalidate()
-            N.check(N.lib().ts_set_field(self._h, st._index, N.FIELDS["h_ext"], h.ctypes.data, h.size))
-            nbytes += h.nbytes
-            full = np.zeros((st.ni + 4, st.nj + 4))
-            full[2:-2, 2:-2] = eta0
-            for f in ("eta_old", "eta_new"):
-                N.check(N.lib().ts_set_field(self._h, st._index, N.FIELDS[f], full.ctypes.data, full.size))
-            nbytes += 2 * eta0.nbytes
+            N.check(L.ts_set_field(self._h, st._index, N.FIELDS["h_ext"], h.ctypes.data, h.size))
+            N.check(L.ts_set_initial_eta(self._h, st._index, eta0.ctypes.data, eta0.size))
+            nbytes += h.nbytes + eta0.nbytes
         return nbytes
 
-    def download_outputs(self):
-        """Device->host read of the results: max_eta, max_speed,
-        max_inundation and the current water level of every block."""
-        out, nbytes = {}, 0
-        for bid, acc in self.accumulators.items():
-            acc._invalidate()
+    def output_buffers(self, pinned: bool = False):
+        """Host buffers for ``download_outputs``: per owned block id
+        (max_eta, max_speed, max_inundation, eta_old), reference shapes."""
+        alloc = N.pinned_empty if pinned else np.empty
+        return {bid: (alloc((st.ni, st.nj)), alloc((st.ni, st.nj)), alloc((st.ni, st.nj)),
+                      alloc((st.ni + 4, st.nj + 4)))
+                for bid, st in self.states.items()}
+
+    def download_outputs(self, out=None):
+        """Device->host read of the results of the owned blocks: max_eta,
+        max_speed, max_inundation and the current water level.  Fills
+        ``out`` (from ``output_buffers``) when given.  Returns (dict, bytes)."""
+        if out is None:
+            out = self.output_buffers()
+        L, nbytes = N.lib(), 0
+        self._sync_in()
+        for bid, bufs in out.items():
             st = self.states[bid]
-            st._invalidate()
-            out[bid] = (acc.max_eta, acc.max_speed, acc.max_inundation, st.eta_old)
-            nbytes += sum(a.nbytes for a in out[bid])
+            for f, a in zip(("max_eta", "max_speed", "max_inundation", "eta_old"), bufs):
+                N.check(L.ts_get_field(self._h, st._index, N.FIELDS[f], a.ctypes.data, a.size))
+                nbytes += a.nbytes
         return out, nbytes
 
     @property

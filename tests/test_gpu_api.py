@@ -150,3 +150,27 @@ def test_message_trace(cuda_device, product, tmp_path):
     assert recs and all(r[2] != r[3] for r in recs)
     assert sorted({r[0] for r in recs}) == [0, 1, 2]
     assert {r[1] for r in recs} <= {0, 1, 2, 3}
+
+
+def test_end_to_end_host_buffers_match_fresh_run(cuda_device, product):
+    """The e2e leg of bench.py: upload of page-locked inputs + run + download
+    into page-locked buffers gives exactly a plain run's state."""
+    from paper_2408_07609_b200.runner import host_block_arrays
+    system, settings, _ = systems.make(product, "quad_wetdry")
+    plan = _plan(product, system, 1)
+    fresh = product.Simulation(system, settings, plan)
+    fresh.run(25, threaded=False)
+    sim = product.Simulation(system, settings, plan)
+    arrays = host_block_arrays(system, settings, pinned=True)
+    nbytes = sim.upload_initial_state(arrays)
+    assert nbytes == sum(a[0].nbytes + a[2].nbytes for a in arrays.values())
+    sim.run(25, threaded=False)
+    outs = sim.output_buffers(pinned=True)
+    got, nb = sim.download_outputs(outs)
+    assert nb == sum(a.nbytes for bufs in outs.values() for a in bufs)
+    for bid, (me, ms, mi, eo) in got.items():
+        acc = fresh.accumulators[bid]
+        assert np.array_equal(me, acc.max_eta)
+        assert np.array_equal(ms, acc.max_speed)
+        assert np.array_equal(mi, acc.max_inundation)
+        assert np.array_equal(eo, fresh.states[bid].eta_old)

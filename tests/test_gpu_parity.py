@@ -177,3 +177,39 @@ def test_kernel_parity_extreme_magnitudes(cuda_device, oracle_mod, product, scal
         orc.phase(ph)
         gpu.phase(ph)
         assert_same(gpu, orc, ph)
+
+
+def test_kochi_six_hours_vs_reference_golden(cuda_device, product):
+    """The 6-hour golden (tests/golden/make_golden_6h.py): the cbrt-aligned
+    reference on Kochi-0.001, digests at 1000 / 10000 / 36000 / 37000 steps,
+    then the reference's own blow-up inside the next 1000 steps with its
+    NumericsError message.  The product must reproduce all of it."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "kochi6h.json")) as f:
+        g = json.load(f)
+    system, settings, _ = systems.kochi(product, 0.001)
+    eta0 = systems.eta0_of(system, settings)
+    if any(systems.digest(eta0[b.block_id]) != g["eta0"][str(b.block_id)] for _, b in system.all_blocks()):
+        pytest.skip("this host's libm (np.exp) differs from the golden host's")
+    sim = product.Simulation(system, settings, _plan(product, system, 1))
+    done = 0
+    for target in sorted(int(k) for k in g["checkpoints"]):
+        sim.run(target - done, threaded=False)
+        done = target
+        want = g["checkpoints"][str(target)]
+        for bid, st in sim.states.items():
+            for f in ("eta_old", "m_old", "n_old"):
+                assert systems.digest(getattr(st, f)) == want[f"{bid}/{f}"], (target, bid, f)
+            for f in ACCS:
+                assert systems.digest(getattr(sim.accumulators[bid], f)) == want[f"{bid}/{f}"], (target, bid, f)
+    acc = np.load(os.path.join(GOLDEN, "kochi6h_acc.npz"))
+    for key in acc.files:
+        bid, f = key.split("/")
+        assert np.array_equal(getattr(sim.accumulators[int(bid)], f), acc[key]), key
+    fail = g["failure"]
+    assert fail is not None and done == fail["after"]
+    with pytest.raises(product.NumericsError) as ei:
+        sim.run(fail["within"], threaded=False)
+    assert str(ei.value) == fail["message"]

@@ -156,3 +156,32 @@ def test_oracle_error_message(oracle_mod, product):
     with pytest.raises(oracle_mod.OracleNumericsError) as ei:
         sim.run(3)
     assert str(ei.value) == want
+
+
+def test_oracle_kochi6h_first_checkpoint(oracle_mod, product):
+    """The 6-hour golden's first checkpoint (1000 steps of Kochi-0.001 on the
+    cbrt-aligned reference); the full 37,000-step run and the reference's
+    blow-up are checked against the product on the GPU, and against the
+    oracle with TSUNAMI_SLOW=1."""
+    with open(os.path.join(GOLDEN, "kochi6h.json")) as f:
+        g = json.load(f)
+    system, settings, _ = systems.kochi(product, 0.001)
+    eta0 = systems.eta0_of(system, settings)
+    if any(systems.digest(eta0[b.block_id]) != g["eta0"][str(b.block_id)] for _, b in system.all_blocks()):
+        pytest.skip("this host's libm (np.exp) differs from the golden host's")
+    sim = oracle_mod.OracleSimulation(system, settings)
+    targets = sorted(int(k) for k in g["checkpoints"])
+    if os.environ.get("TSUNAMI_SLOW") != "1":
+        targets = targets[:1]
+    done = 0
+    for target in targets:
+        sim.run(target - done)
+        done = target
+        want = g["checkpoints"][str(target)]
+        for bid, st in sim.states.items():
+            for f in ("eta_old", "m_old", "n_old") + ACCS:
+                assert systems.digest(getattr(st, f)) == want[f"{bid}/{f}"], (target, bid, f)
+    if os.environ.get("TSUNAMI_SLOW") == "1":
+        with pytest.raises(oracle_mod.OracleNumericsError) as ei:
+            sim.run(g["failure"]["within"])
+        assert str(ei.value) == g["failure"]["message"]
