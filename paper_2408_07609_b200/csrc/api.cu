@@ -78,6 +78,10 @@ struct ts_handle {
     bool mom_par = true;
     cudaStream_t side[3] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[3] = {};
+    // contiguous device staging of host transfers (one 1-D copy + repitch
+    // kernel instead of a row-by-row 2-D copy of narrow rows)
+    double *d_io = nullptr;
+    size_t io_len = 0;
     // multi-GPU (one process per GPU): peer arenas mapped by CUDA IPC
     unsigned long long *d_sig = nullptr;  // [0, nranks): peers' epochs; [nranks]: own epoch
     std::vector<char *> peer_arena;
@@ -299,6 +303,18 @@ struct FieldGeom {
     int rows, cols;     // reference shape
     int pitch;          // device pitch (doubles)
 };
+
+int io_reserve(ts_handle *h, size_t n)
+{
+    if (n <= h->io_len) return TS_OK;
+    CK(cudaStreamSynchronize(h->stream));
+    if (h->d_io) CK(cudaFree(h->d_io));
+    h->d_io = nullptr;
+    h->io_len = 0;
+    CK(cudaMalloc((void **)&h->d_io, n * 8));
+    h->io_len = n;
+    return TS_OK;
+}
 
 int field_geom(ts_handle *h, int b, int field, FieldGeom *g)
 {
@@ -936,9 +952,11 @@ int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_
     if (int rc = field_geom(h, block, field, &g)) return rc;
     if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
     CK(cudaSetDevice(h->device));
+    if (int rc = io_reserve(h, (size_t)len)) return rc;
+    launch_repitch(h->d_io, g.cols, g.ptr, g.pitch, g.rows, g.cols, h->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, h->d_io, (size_t)len * 8, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy2D(out, (size_t)g.cols * 8, g.ptr, (size_t)g.pitch * 8, (size_t)g.cols * 8, g.rows,
-                    cudaMemcpyDeviceToHost));
     return TS_OK;
 }
 
@@ -949,9 +967,11 @@ int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, i
     if (int rc = field_geom(h, block, field, &g)) return rc;
     if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
     CK(cudaSetDevice(h->device));
+    if (int rc = io_reserve(h, (size_t)len)) return rc;
+    CK(cudaMemcpyAsync(h->d_io, in, (size_t)len * 8, cudaMemcpyHostToDevice, h->stream));
+    launch_repitch(g.ptr, g.pitch, h->d_io, g.cols, g.rows, g.cols, h->stream);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(h->stream));
-    CK(cudaMemcpy2D(g.ptr, (size_t)g.pitch * 8, in, (size_t)g.cols * 8, (size_t)g.cols * 8, g.rows,
-                    cudaMemcpyHostToDevice));
     return TS_OK;
 }
 
@@ -963,10 +983,12 @@ int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t 
     const DevBlock &B = h->hb[block];
     if (len != (int64_t)B.ni * B.nj) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, B.ni, B.nj);
     CK(cudaSetDevice(h->device));
-    CK(cudaStreamSynchronize(h->stream));
+    if (int rc = io_reserve(h, (size_t)len)) return rc;
+    CK(cudaMemcpyAsync(h->d_io, eta0, (size_t)len * 8, cudaMemcpyHostToDevice, h->stream));
     for (int k = 0; k < 2; ++k)
-        CK(cudaMemcpy2D(B.eta[k] + 2 * (size_t)B.P + 2, (size_t)B.P * 8, eta0, (size_t)B.nj * 8,
-                        (size_t)B.nj * 8, B.ni, cudaMemcpyHostToDevice));
+        launch_repitch(B.eta[k] + 2 * (size_t)B.P + 2, B.P, h->d_io, B.nj, B.ni, B.nj, h->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
     return TS_OK;
 }
 
@@ -1050,6 +1072,7 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_hflux);
     cudaFree(h->d_edge);
     cudaFree(h->d_stage);
+    cudaFree(h->d_io);
     cudaFree(h->d_err);
     cudaFree(h->d_accflag);
     cudaFree(h->d_blocks);

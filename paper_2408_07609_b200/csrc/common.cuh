@@ -107,3 +107,5 @@ void launch_prolong(const StepArgs &a, const PSeg *segs, int nseg, int64_t nelem
                     int mode, cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
+void launch_repitch(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols,
+                    cudaStream_t s);
