@@ -90,6 +90,8 @@ struct ts_handle {
     int imported = 0;
     bool x_restrict = false, x_halo = false, x_prolong = false;   // cross-rank traffic per phase
     RSeg *d_rseg = nullptr;
+    int2 *d_rchunk = nullptr, *d_pchunk = nullptr;    // (segment, first element) per CTA
+    int n_rchunk = 0, n_pchunk = 0;
     int n_rseg = 0;
     int64_t r_elems = 0;
     bool r_two_pass = false;
@@ -188,12 +190,12 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (h->x_restrict) { barrier(h, s); ++n; }
     if (h->r_elems || h->x_restrict) {
         if (h->r_two_pass) {
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 1, s);
             if (h->x_restrict) { barrier(h, s); ++n; }
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 2, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 2, s);
             n += 2;
         } else {
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, nullptr, 0, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, nullptr, 0, s);
             ++n;
         }
     }
@@ -235,12 +237,12 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (h->x_prolong) { barrier(h, s); ++n; }
     if (h->p_elems || h->x_prolong) {
         if (h->p_two_pass) {
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 1, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 1, s);
             if (h->x_prolong) { barrier(h, s); ++n; }
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 2, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 2, s);
             n += 2;
         } else {
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, nullptr, 0, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, nullptr, 0, s);
             ++n;
         }
     }
@@ -619,6 +621,11 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->n_rseg = (int)segs.size();
         stage_len = std::max(stage_len, (size_t)first);
         if (int rc = upload(&h->d_rseg, segs)) return rc;
+        std::vector<int2> ch;
+        for (int q = 0; q < (int)segs.size(); ++q)
+            for (int o = 0; o < segs[q].count; o += 256) ch.push_back(make_int2(q, o));
+        h->n_rchunk = (int)ch.size();
+        if (int rc = upload(&h->d_rchunk, ch)) return rc;
     }
     // ---- prolongation segments (coupling.py:318-340)
     {
@@ -659,6 +666,11 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->n_pseg = (int)segs.size();
         stage_len = std::max(stage_len, (size_t)first);
         if (int rc = upload(&h->d_pseg, segs)) return rc;
+        std::vector<int2> ch;
+        for (int q = 0; q < (int)segs.size(); ++q)
+            for (int o = 0; o < 3 * segs[q].count; o += 256) ch.push_back(make_int2(q, o));
+        h->n_pchunk = (int)ch.size();
+        if (int rc = upload(&h->d_pchunk, ch)) return rc;
     }
     if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
 
@@ -910,10 +922,10 @@ int ts_phase(ts_handle *h, int32_t phase)
     case TS_PH_MASS: launch_mass(a, h->d_all, h->n_all, false, s); break;
     case TS_PH_RESTRICT:
         if (h->r_two_pass) {
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 1, s);
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, h->d_stage, 2, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 1, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 2, s);
         } else {
-            launch_restrict(a, h->d_rseg, h->n_rseg, h->r_elems, nullptr, 0, s);
+            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, nullptr, 0, s);
         }
         break;
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
@@ -927,10 +939,10 @@ int ts_phase(ts_handle *h, int32_t phase)
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
     case TS_PH_PROLONG:
         if (h->p_two_pass) {
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 1, s);
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, h->d_stage, 2, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 1, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 2, s);
         } else {
-            launch_prolong(a, h->d_pseg, h->n_pseg, h->p_elems, nullptr, 0, s);
+            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, nullptr, 0, s);
         }
         break;
     case TS_PH_HALO_FLUX: launch_copies(a, h->d_hflux, h->n_hflux, false, s); break;
@@ -1068,6 +1080,8 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_err_next);
     cudaFree(h->d_rseg);
     cudaFree(h->d_pseg);
+    cudaFree(h->d_rchunk);
+    cudaFree(h->d_pchunk);
     cudaFree(h->d_heta);
     cudaFree(h->d_hflux);
     cudaFree(h->d_edge);

@@ -8,6 +8,7 @@
 // [-2, n+2)) sits at (x+2)*P + (y+2); M face (fx, cy) at (fx+2)*P + cy+2;
 // N (cx, fy) at (cx+2)*P + fy+2; accumulators (i, j) at i*P + j.
 #pragma once
+#include <cuda_runtime.h>
 #include <stdint.h>
 
 #define TS_G 2
@@ -101,9 +102,9 @@ void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStr
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fuse,
                      cudaStream_t s);
 void launch_promote(const StepArgs &a, cudaStream_t s);
-void launch_restrict(const StepArgs &a, const RSeg *segs, int nseg, int64_t nelem, double *stage,
+void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
                      int mode, cudaStream_t s);
-void launch_prolong(const StepArgs &a, const PSeg *segs, int nseg, int64_t nelem, double *stage,
+void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int nchunks, double *stage,
                     int mode, cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
