@@ -195,7 +195,10 @@ def run_ours(args):
     cells = system.cell_count
     counts = [b.cell_count for _, b in system.all_blocks()]
     # blocks -> GPUs: exact min-max partition of the level-ordered block list
-    plan = P.minmax_plan(counts, world) if world > 1 else P.equal_cell_plan(counts, 1)
+    # under the B200 per-block cost (cells for the mass pass, marched lanes
+    # for the momentum pass)
+    plan = (P.minmax_plan(counts, world, weights=P.b200_block_weights(system)) if world > 1
+            else P.equal_cell_plan(counts, 1))
     sim = P.Simulation(system, settings, plan, device=local, distributed=world > 1)
     ext = torch.cuda.ExternalStream(sim.stream_ptr, device=local)
     sim.run(args.warmup, threaded=False)
@@ -214,6 +217,11 @@ def run_ours(args):
     t = D.max_over_ranks(t_local) if world > 1 else t_local
     mass_s, mom_s, step_s = sim.kernel_seconds()
     launches = sim.launches_per_step * args.steps + 4
+    my_cells = sum(c for k, c in enumerate(counts) if sim.owner[k] == rank)
+    per_rank = [(rank, my_cells, mass_s, mom_s, step_s)]
+    if world > 1:
+        import pickle
+        per_rank = [pickle.loads(b) for b in D.all_gather_bytes(pickle.dumps(per_rank[0]))]
 
     # end to end through the public API with host buffers: upload the host
     # inputs, K steps, download the result maps (every rank its own blocks)
@@ -232,7 +240,6 @@ def run_ours(args):
         d2h = sum(D.all_gather_bytes(d2h))
 
     peak, peak_src = measured_peaks()
-    my_cells = sum(c for k, c in enumerate(counts) if sim.owner[k] == rank)
     achieved = ALG_BYTES_MOM * my_cells / mom_s / 1e9 if mom_s > 0 else None
     traffic = profiled_traffic() if world == 1 else None   # the capture is of the 1-GPU step
     line = {
@@ -258,6 +265,8 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "wall_s": te},
         "gpu_launches": launches,
+        "ranks": [{"rank": r, "cells": c, "mass_s": m, "momentum_s": k, "step_s": st}
+                  for r, c, m, k, st in per_rank],
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu and world == 1:

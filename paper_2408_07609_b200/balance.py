@@ -130,14 +130,34 @@ def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
     return DecompositionPlan(cells, tuple(seps))
 
 
-def minmax_plan(cells, n_ranks: int, model: CostModel = B200_MODEL) -> DecompositionPlan:
+def b200_block_weights(system, tile_rows: int = 64, mom_share: float = 0.68) -> list:
+    """Relative B200 step cost of every block (global order).  The mass pass
+    costs per cell; the momentum march costs per marched lane-row: a block of
+    width nj runs ceil((nj + 3) / 32) warps per tile (column tiles of 126
+    faces above 125) over ni + 1 face rows plus two extra rows per tile."""
+    out = []
+    for _, b in system.all_blocks():
+        ni, nj = b.ni, b.nj
+        if nj + 3 <= 128:
+            lanes = 32 * ((nj + 3 + 31) // 32)
+        else:
+            lanes = 128 * ((nj + 1 + 125) // 126)
+        tiles = (ni + 1 + tile_rows - 1) // tile_rows
+        march = lanes * (ni + 1 + 2 * tiles) / (nj + 1)      # lane-rows per output column
+        out.append(mom_share * march + (1.0 - mom_share) * ni)
+    return [w * b.nj for w, (_, b) in zip(out, system.all_blocks())]
+
+
+def minmax_plan(cells, n_ranks: int, model: CostModel = B200_MODEL, weights=None) -> DecompositionPlan:
     """Exact minimum of the maximum per-rank cost over all consecutive
-    partitions into exactly ``n_ranks`` non-empty runs (O(n^2 k) DP)."""
+    partitions into exactly ``n_ranks`` non-empty runs (O(n^2 k) DP).  The
+    per-block cost is ``model.block_cost(cells)``, or ``weights`` when given
+    (e.g. ``b200_block_weights``)."""
     cells = tuple(int(c) for c in cells)
     n = len(cells)
     if not 1 <= n_ranks <= n:
         raise PlanError(f"{n_ranks} ranks infeasible for {n} blocks")
-    cost = np.asarray(model.block_cost(cells), dtype=float)
+    cost = np.asarray(model.block_cost(cells) if weights is None else weights, dtype=float)
     pre = np.concatenate([[0.0], np.cumsum(cost)])
     INF = float("inf")
     best = np.full((n_ranks + 1, n + 1), INF)
