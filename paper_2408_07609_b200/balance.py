@@ -130,22 +130,36 @@ def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
     return DecompositionPlan(cells, tuple(seps))
 
 
-def b200_block_weights(system, tile_rows: int = 64, mom_share: float = 0.68) -> list:
-    """Relative B200 step cost of every block (global order).  The mass pass
-    costs per cell; the momentum march costs per marched lane-row: a block of
-    width nj runs ceil((nj + 3) / 32) warps per tile (column tiles of 126
-    faces above 125) over ni + 1 face rows plus two extra rows per tile."""
-    out = []
-    for _, b in system.all_blocks():
-        ni, nj = b.ni, b.nj
-        if nj + 3 <= 128:
-            lanes = 32 * ((nj + 3 + 31) // 32)
-        else:
-            lanes = 128 * ((nj + 1 + 125) // 126)
-        tiles = (ni + 1 + tile_rows - 1) // tile_rows
-        march = lanes * (ni + 1 + 2 * tiles) / (nj + 1)      # lane-rows per output column
-        out.append(mom_share * march + (1.0 - mom_share) * ni)
-    return [w * b.nj for w, (_, b) in zip(out, system.all_blocks())]
+# Measured B200 step cost per cell (ps) by block width: tools/fit_costs.py
+# (single-level systems of ~8 M cells of one width; mass + momentum + the
+# small kernels, round-1 kernels).  The march runs ceil((nj+3)/32) warps per
+# tile, so narrow or just-over-a-warp widths cost more per cell.
+B200_STEP_PS_BY_WIDTH = {24: 61.4, 36: 68.2, 48: 56.1, 60: 51.4, 90: 54.9}
+
+
+def _lane_factor(nj: int) -> float:
+    lanes = 32 * ((nj + 3 + 31) // 32) if nj + 3 <= 128 else 128 * ((nj + 1 + 125) // 126)
+    return lanes / (nj + 1)
+
+
+def b200_step_ps_per_cell(nj: int, table=None) -> float:
+    """Per-cell step cost of a block of width nj: the measured table, else
+    the march's lane utilisation scaled to the table (2/3 of the step is the
+    march, 1/3 is per-cell memory work)."""
+    table = B200_STEP_PS_BY_WIDTH if table is None else table
+    if nj in table:
+        return float(table[nj])
+    ref = min(table, key=lambda w: abs(w - 60)) if table else 60
+    base = float(table.get(ref, 51.4))
+    return base * (2.0 * _lane_factor(nj) / _lane_factor(ref) + 1.0) / 3.0
+
+
+def b200_block_weights(system, table=None, block_overhead_ps: float = 0.0) -> list:
+    """Relative B200 step cost of every block (global order), for
+    ``minmax_plan(..., weights=...)``: cells x the per-cell cost of the
+    block's width (+ a per-block overhead)."""
+    return [b.ni * b.nj * b200_step_ps_per_cell(b.nj, table) + block_overhead_ps
+            for _, b in system.all_blocks()]
 
 
 def minmax_plan(cells, n_ranks: int, model: CostModel = B200_MODEL, weights=None) -> DecompositionPlan:

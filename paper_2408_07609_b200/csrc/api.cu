@@ -1004,6 +1004,10 @@ int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t 
     return TS_OK;
 }
 
+// guard-failure counters of a -DTS_DEBUG=1 build (0 elsewhere); not in the
+// public header
+extern "C" int ts_debug_counters(unsigned long long *out, int n) { return debug_counters(out, n); }
+
 void *ts_host_alloc(int64_t bytes)
 {
     void *p = nullptr;

@@ -108,5 +108,6 @@ void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int
                     int mode, cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
+int debug_counters(unsigned long long *out, int n);
 void launch_repitch(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols,
                     cudaStream_t s);
