@@ -51,6 +51,7 @@ struct Group {
     int W = 0;
     std::vector<Tile> tiles;
     Tile *d = nullptr;
+    unsigned char *dirty = nullptr;     // per-CTA flags when momentum_split(W)
 };
 
 }  // namespace
@@ -223,8 +224,8 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
                 st = h->side[x - 1];
                 CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
             }
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, st);
-            ++n;
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, gr.dirty, st);
+            n += (gr.dirty && !(variant & kFuse)) ? 2 : 1;
             if (par && x > 0) {
                 CK(cudaEventRecord(h->ev_join[x - 1], st));
                 CK(cudaStreamWaitEvent(s, h->ev_join[x - 1], 0));
@@ -558,6 +559,12 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     for (auto &gr : h->groups) {
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
+        if (!gr.tiles.empty() && momentum_split(gr.W)) {
+            const int tpc = momentum_tiles_per_cta(gr.W);
+            const size_t n = (gr.tiles.size() + tpc - 1) / tpc;
+            CK(cudaMalloc((void **)&gr.dirty, n));
+            CK(cudaMemset(gr.dirty, 0, n));
+        }
     }
     {
         // cell tiles of the flat kernels (mass + fold, flush): about
@@ -933,7 +940,7 @@ int ts_phase(ts_handle *h, int32_t phase)
         for (int k = 0; k < 4; ++k) {
             Group &gr = h->groups[k];
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, gr.dirty, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
@@ -1078,6 +1085,7 @@ void ts_destroy(ts_handle *h)
             if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) {
         cudaFree(gr.d);
+        cudaFree(gr.dirty);
     }
     cudaFree(h->d_all);
     cudaFree(h->d_perim);

@@ -100,7 +100,9 @@ void launch_barrier(const BarrierArgs &b, cudaStream_t s);
 void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fuse,
-                     cudaStream_t s);
+                     unsigned char *dirty, cudaStream_t s);
+bool momentum_split(int W);     // the width-W group uses per-CTA dirty flags
+int momentum_tiles_per_cta(int W);
 void launch_promote(const StepArgs &a, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
                      int mode, cudaStream_t s);
