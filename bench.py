@@ -63,6 +63,9 @@ def build_workload(P, name, scale):
     if name in ("cfg1", "cfg2"):
         system, settings, _ = systems.make(P, name)
         return system, settings, f"{name} (BASELINE config {name[-1]})"
+    if name == "cfg5":
+        system, settings, _ = systems.cfg5(P, scale)
+        return system, settings, f"cfg5 single-level 10 m, {system.cell_count} cells in 8 strips (BASELINE config 5)"
     raise SystemExit(f"unknown config {name}")
 
 
@@ -140,6 +143,21 @@ def profiled_traffic():
         return None
 
 
+def profiled_fp64():
+    """FP64-pipe utilisation of the widest-group march launch in the
+    committed ncu capture (the kernel is FP64-issue bound, not HBM bound)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_full.json")) as f:
+            ks = json.load(f)["kernels"]
+        k = max((k for k in ks if "march" in k["kernel"]), key=lambda k: k["gpu__time_duration.sum"])
+        return {"kernel": k["kernel"], "fp64_pipe_active_frac":
+                k["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"] / 100.0,
+                "issue_active_frac": k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0,
+                "source": "profiles/r01_ncu_full.json"}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def cpu_sample(system, settings, steps=2, warm=1):
     """The oracle on ``steps`` steps of the same workload, all host threads."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -194,11 +212,10 @@ def run_ours(args):
     system, settings, label = build_workload(P, args.config, args.scale)
     cells = system.cell_count
     counts = [b.cell_count for _, b in system.all_blocks()]
-    # blocks -> GPUs: exact min-max partition of the level-ordered block list
-    # under the B200 per-block cost (cells for the mass pass, marched lanes
-    # for the momentum pass)
-    plan = (P.minmax_plan(counts, world, weights=P.b200_block_weights(system)) if world > 1
-            else P.equal_cell_plan(counts, 1))
+    # blocks -> GPUs: consecutive runs of the level-ordered block list
+    # balancing the mass and the momentum phase separately under the
+    # measured B200 per-width costs (balance.phase_balanced_plan)
+    plan = P.phase_balanced_plan(system, world) if world > 1 else P.equal_cell_plan(counts, 1)
     sim = P.Simulation(system, settings, plan, device=local, distributed=world > 1)
     ext = torch.cuda.ExternalStream(sim.stream_ptr, device=local)
     sim.run(args.warmup, threaded=False)
@@ -250,7 +267,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cells": cells, "levels": len(system.levels),
                    "blocks": system.n_blocks, "dt_s": settings.dt,
-                   "parallelism": f"blocks over {world} GPU(s) (min-max plan {list(plan.separators)})",
+                   "parallelism": f"blocks over {world} GPU(s) (phase-balanced plan {list(plan.separators)})",
                    "l2": "state 3.8 GB >> 126 MB L2; no flush"},
         "six_hour_wall_s": t / args.steps * SIX_HOURS_STEPS,
         "step_roofline": {"bytes_per_cell_step": ALG_BYTES_STEP,
@@ -260,7 +277,8 @@ def run_ours(args):
                      "unit": "GB/s", "frac": achieved / peak if achieved else None,
                      "traffic": traffic, "alg_bytes_per_launch": ALG_BYTES_MOM * my_cells,
                      "avg_launch_s": mom_s, "peak_source": peak_src,
-                     "mass_kernel_s": mass_s, "step_s_events": step_s, "rank": rank},
+                     "mass_kernel_s": mass_s, "step_s_events": step_s, "rank": rank,
+                     "fp64": profiled_fp64()},
         "e2e": {"value": cells * args.steps / te / 1e9, "unit": "Gcell/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "wall_s": te},

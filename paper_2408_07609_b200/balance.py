@@ -130,11 +130,14 @@ def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
     return DecompositionPlan(cells, tuple(seps))
 
 
-# Measured B200 step cost per cell (ps) by block width: tools/fit_costs.py
-# (single-level systems of ~8 M cells of one width; mass + momentum + the
-# small kernels, round-1 kernels).  The march runs ceil((nj+3)/32) warps per
-# tile, so narrow or just-over-a-warp widths cost more per cell.
-B200_STEP_PS_BY_WIDTH = {24: 61.4, 36: 68.2, 48: 56.1, 60: 51.4, 90: 54.9}
+# Measured B200 cost per cell (ps) by block width: tools/fit_costs.py
+# (single-level systems of 40 M cells of one width, 30 steps; round-1
+# kernels).  The
+# march runs ceil((nj+3)/32) warps per tile, so widths just past a warp
+# multiple cost more per cell; the mass pass is per-cell memory work.
+B200_MASS_PS_BY_WIDTH = {24: 15.19, 36: 14.4, 48: 13.8, 60: 13.58, 90: 13.65}
+B200_MOMENTUM_PS_BY_WIDTH = {24: 36.88, 36: 48.72, 48: 36.77, 60: 29.53, 90: 29.6}
+B200_STEP_PS_BY_WIDTH = {24: 55.16, 36: 65.59, 48: 52.55, 60: 44.69, 90: 44.61}
 
 
 def _lane_factor(nj: int) -> float:
@@ -152,6 +155,59 @@ def b200_step_ps_per_cell(nj: int, table=None) -> float:
     ref = min(table, key=lambda w: abs(w - 60)) if table else 60
     base = float(table.get(ref, 51.4))
     return base * (2.0 * _lane_factor(nj) / _lane_factor(ref) + 1.0) / 3.0
+
+
+def b200_phase_weights(system):
+    """(mass, momentum) B200 cost of every block (global order), ps/step."""
+    mass, mom = [], []
+    for _, b in system.all_blocks():
+        n = b.ni * b.nj
+        mass.append(n * B200_MASS_PS_BY_WIDTH.get(b.nj, 13.7))
+        if b.nj in B200_MOMENTUM_PS_BY_WIDTH:
+            mom.append(n * B200_MOMENTUM_PS_BY_WIDTH[b.nj])
+        else:
+            mom.append(n * 29.53 * _lane_factor(b.nj) / _lane_factor(60))
+    return mass, mom
+
+
+def _phase_objective(seps, mass, mom):
+    cuts = (0, *seps, len(mass))
+    pm = [sum(mass[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    pk = [sum(mom[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
+    # the step runs the phases between rank barriers: the slowest rank of
+    # each phase sets the pace (ties broken towards the balanced total)
+    return max(pm) + max(pk) + 1e-3 * max(x + y for x, y in zip(pm, pk))
+
+
+def phase_balanced_plan(system, n_ranks: int) -> DecompositionPlan:
+    """Consecutive-block plan minimising max(mass) + max(momentum) over
+    ranks (the step's two big phases are separated by rank barriers, so
+    balancing their sum is not enough): exhaustive for two ranks, else
+    separator-wise descent from the min-max plan of the summed cost."""
+    cells = tuple(b.ni * b.nj for _, b in system.all_blocks())
+    mass, mom = b200_phase_weights(system)
+    n = len(cells)
+    if n_ranks == 1:
+        return DecompositionPlan(cells, ())
+    if n_ranks == 2:
+        best = min(range(1, n), key=lambda s: _phase_objective((s,), mass, mom))
+        return DecompositionPlan(cells, (best,))
+    seps = list(minmax_plan(cells, n_ranks, weights=[a + b for a, b in zip(mass, mom)]).separators)
+    cur = _phase_objective(seps, mass, mom)
+    improved = True
+    while improved:
+        improved = False
+        for k in range(len(seps)):
+            lo = seps[k - 1] + 1 if k else 1
+            hi = seps[k + 1] - 1 if k + 1 < len(seps) else n - 1
+            for v in range(lo, hi + 1):
+                if v == seps[k]:
+                    continue
+                trial = seps[:k] + [v] + seps[k + 1:]
+                j = _phase_objective(trial, mass, mom)
+                if j < cur - 1e-9:
+                    seps, cur, improved = trial, j, True
+    return DecompositionPlan(cells, tuple(seps))
 
 
 def b200_block_weights(system, table=None, block_overhead_ps: float = 0.0) -> list:

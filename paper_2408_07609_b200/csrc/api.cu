@@ -11,6 +11,7 @@
 #include <string>
 #include <unordered_map>
 #include <unordered_set>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/tsunami_b200.h"
@@ -46,6 +47,13 @@ constexpr int kPhaseEvents = 8;
 // boundaries retargeted per step in timing mode: mass (0,1), momentum (3,4),
 // whole step (0,7)
 constexpr int kTimed[5] = {0, 1, 3, 4, 7};
+
+template <typename S>
+struct SegList {
+    S *d = nullptr;
+    int2 *ch = nullptr;       // (segment, first element) per CTA
+    int nch = 0;
+};
 
 struct Group {
     int W = 0;
@@ -90,15 +98,15 @@ struct ts_handle {
     unsigned long long **d_peer_sig = nullptr;
     int imported = 0;
     bool x_restrict = false, x_halo = false, x_prolong = false;   // cross-rank traffic per phase
-    RSeg *d_rseg = nullptr;
-    int2 *d_rchunk = nullptr, *d_pchunk = nullptr;    // (segment, first element) per CTA
-    int n_rchunk = 0, n_pchunk = 0;
-    int n_rseg = 0;
-    int64_t r_elems = 0;
+    // coupling segment lists: send = this rank's sources (direct, or into the
+    // local stage / a peer's receive area), local = second pass of a two-pass
+    // exchange, recv = cross-rank values received into this rank's area
+    SegList<RSeg> r_send, r_local, r_recv;
+    SegList<PSeg> p_send, p_local, p_recv;
+    std::vector<size_t> recv_off;         // byte offset of every owner's receive area in its arena
+    double **d_recv = nullptr;            // [n_ranks] receive-area bases (own + mapped peers)
+    std::vector<double *> recv_base;
     bool r_two_pass = false;
-    PSeg *d_pseg = nullptr;
-    int n_pseg = 0;
-    int64_t p_elems = 0;
     bool p_two_pass = false;
     Copy *d_heta = nullptr, *d_hflux = nullptr, *d_edge = nullptr;
     int64_t n_heta = 0, n_hflux = 0, n_edge = 0;
@@ -137,6 +145,7 @@ StepArgs args_of(const ts_handle *h, int cur)
     a.err_next = h->d_err_next;
     a.acc_flag = h->d_accflag;
     a.multi = h->nranks > 1;
+    a.recv = h->d_recv;
     return a;
 }
 
@@ -188,19 +197,13 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     // multi-GPU phase barriers: only around phases with
     // cross-rank stores; each one orders this rank's peer stores before the
     // readers' next phase and keeps writers from overtaking readers
+    // restriction: this rank's sources (direct / staged / into peers'
+    // receive areas), the second pass of a two-pass exchange, then - once
+    // every rank's stores have landed - the values received from peers
+    if (h->r_send.nch) { launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, s); ++n; }
+    if (h->r_local.nch) { launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, s); ++n; }
     if (h->x_restrict) { barrier(h, s); ++n; }
-    if (h->r_elems || h->x_restrict) {
-        if (h->r_two_pass) {
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 1, s);
-            if (h->x_restrict) { barrier(h, s); ++n; }
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 2, s);
-            n += 2;
-        } else {
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, nullptr, 0, s);
-            ++n;
-        }
-    }
-    if (h->x_restrict) { barrier(h, s); ++n; }
+    if (h->r_recv.nch) { launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, s); ++n; }
     if (mark(2)) return TS_ERR_CUDA;
     if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
     if (h->x_halo) { barrier(h, s); ++n; }
@@ -235,19 +238,10 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
     if (mark(5)) return TS_ERR_CUDA;
+    if (h->p_send.nch) { launch_prolong(a, h->p_send.d, h->p_send.ch, h->p_send.nch, h->d_stage, s); ++n; }
+    if (h->p_local.nch) { launch_prolong(a, h->p_local.d, h->p_local.ch, h->p_local.nch, h->d_stage, s); ++n; }
     if (h->x_prolong) { barrier(h, s); ++n; }
-    if (h->p_elems || h->x_prolong) {
-        if (h->p_two_pass) {
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 1, s);
-            if (h->x_prolong) { barrier(h, s); ++n; }
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 2, s);
-            n += 2;
-        } else {
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, nullptr, 0, s);
-            ++n;
-        }
-    }
-    if (h->x_prolong) { barrier(h, s); ++n; }
+    if (h->p_recv.nch) { launch_prolong(a, h->p_recv.d, h->p_recv.ch, h->p_recv.nch, h->d_stage, s); ++n; }
     if (mark(6)) return TS_ERR_CUDA;
     if (h->n_hflux) { launch_copies(a, h->d_hflux, h->n_hflux, false, s); ++n; }
     // "output" is folded into the next step's K_mass (and the end-of-run
@@ -480,6 +474,28 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->off[b] = owner_total[bd.owner];
         owner_total[bd.owner] += need;
     }
+    // receive areas of the cross-rank coupling (restriction values, then
+    // prolongation values, in global segment order), after the blocks
+    {
+        std::vector<size_t> relems(h->nranks, 0);
+        for (int k = 0; k < d->n_restrict; ++k) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            if (sg.parent < 0 || sg.parent >= h->nb || sg.child < 0 || sg.child >= h->nb) continue;
+            const int op = d->blocks[sg.parent].owner;
+            if (d->blocks[sg.child].owner != op && sg.parent_hi > sg.parent_lo) relems[op] += sg.parent_hi - sg.parent_lo;
+        }
+        for (int k = 0; k < d->n_prolong; ++k) {
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            if (sg.parent < 0 || sg.parent >= h->nb || sg.child < 0 || sg.child >= h->nb) continue;
+            const int oc = d->blocks[sg.child].owner;
+            if (d->blocks[sg.parent].owner != oc && sg.parent_hi > sg.parent_lo) relems[oc] += 3 * (size_t)(sg.parent_hi - sg.parent_lo);
+        }
+        h->recv_off.assign(h->nranks, 0);
+        for (int o = 0; o < h->nranks; ++o) {
+            h->recv_off[o] = owner_total[o];
+            owner_total[o] += align_up(relems[o] * 8, 256);
+        }
+    }
     const size_t total = owner_total[h->rank];
     h->arena_bytes = total;
     if (total) {
@@ -591,94 +607,134 @@ int create_impl(const ts_desc *d, ts_handle *h)
     auto check_blk = [&](int b) { return b >= 0 && b < h->nb; };
     size_t stage_len = 0;
 
-    // ---- restriction segments (coupling.py:278-315)
+    // ---- coupling segments (coupling.py:278-340).  Pass 1 validates,
+    // flags cross-rank traffic and detects whether any written element is
+    // also read in the same exchange (then the reference's pack-all-then-
+    // apply order needs two passes); pass 2 builds this rank's lists.
+    std::vector<size_t> recv_cur(h->nranks, 0);      // elements, per receiving owner
+    auto build_lists = [&](auto &send, auto &local, auto &recv, auto make, int nseg, auto geom,
+                           bool two_pass, int mult) -> int {
+        using S = typename std::decay<decltype(make(0, 0, 0, 0))>::type;
+        std::vector<S> vs, vl, vr;
+        int64_t stage_cur = 0;
+        for (int k = 0; k < nseg; ++k) {
+            int src, dst, count;
+            geom(k, src, dst, count);
+            if (count == 0) continue;
+            const int os = d->blocks[src].owner, od = d->blocks[dst].owner;
+            const int64_t n = (int64_t)mult * count;
+            int64_t roff = -1;
+            if (os != od) {
+                roff = (int64_t)recv_cur[od];
+                recv_cur[od] += (size_t)n;
+            }
+            if (os == h->rank) {
+                if (os != od) vs.push_back(make(k, 1, od, roff));
+                else if (two_pass) {
+                    vs.push_back(make(k, 1, -1, stage_cur));
+                    vl.push_back(make(k, 2, -1, stage_cur));
+                    stage_cur += n;
+                } else {
+                    vs.push_back(make(k, 0, -1, 0));
+                }
+            } else if (od == h->rank) {
+                vr.push_back(make(k, 2, h->rank, roff));
+            }
+        }
+        stage_len = std::max(stage_len, (size_t)stage_cur);
+        auto up = [&](auto &L, std::vector<S> &v) -> int {
+            if (int rc = upload(&L.d, v)) return rc;
+            std::vector<int2> ch;
+            for (int q = 0; q < (int)v.size(); ++q)
+                for (int o = 0; o < mult * v[q].count; o += 256) ch.push_back(make_int2(q, o));
+            L.nch = (int)ch.size();
+            return upload(&L.ch, ch);
+        };
+        if (int rc = up(send, vs)) return rc;
+        if (int rc = up(local, vl)) return rc;
+        return up(recv, vr);
+    };
     {
-        std::vector<RSeg> segs;
         std::unordered_set<long long> written, read;
         auto key = [](int b, int x, int y) { return ((long long)b << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8); };
-        int64_t first = 0;
         for (int k = 0; k < d->n_restrict; ++k) {
-            const ts_eta_segment &s = d->restrict_segs[k];
-            if (!check_blk(s.parent) || !check_blk(s.child) || s.side < 0 || s.side > 3)
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            if (!check_blk(sg.parent) || !check_blk(sg.child) || sg.side < 0 || sg.side > 3)
                 return fail(TS_ERR_INVALID, "bad restriction segment %d", k);
-            const int count = s.parent_hi - s.parent_lo;
-            if (count < 0 || s.child_hi - s.child_lo != 3 * count)
+            const int count = sg.parent_hi - sg.parent_lo;
+            if (count < 0 || sg.child_hi - sg.child_lo != 3 * count)
                 return fail(TS_ERR_INVALID, "restriction segment %d: spans disagree", k);
             if (count == 0) continue;
-            const bool ns = s.side >= TS_SOUTH;
-            if (d->blocks[s.child].owner != d->blocks[s.parent].owner) h->x_restrict = true;
-            if (owned(s.child)) {
-                segs.push_back(RSeg{s.child, s.parent, ns, s.child_lo, s.ring_start, s.parent_line,
-                                    s.parent_lo, count, first});
-                first += count;
-            }
+            const bool ns = sg.side >= TS_SOUTH;
+            if (d->blocks[sg.child].owner != d->blocks[sg.parent].owner) h->x_restrict = true;
             for (int p = 0; p < count; ++p) {
-                written.insert(key(s.parent, ns ? s.parent_lo + p : s.parent_line, ns ? s.parent_line : s.parent_lo + p));
+                written.insert(key(sg.parent, ns ? sg.parent_lo + p : sg.parent_line, ns ? sg.parent_line : sg.parent_lo + p));
                 for (int u = 0; u < 3; ++u)
                     for (int v = 0; v < 3; ++v) {
-                        const int x = ns ? s.child_lo + 3 * p + u : s.ring_start + u;
-                        const int y = ns ? s.ring_start + v : s.child_lo + 3 * p + v;
-                        read.insert(key(s.child, x, y));
+                        const int x = ns ? sg.child_lo + 3 * p + u : sg.ring_start + u;
+                        const int y = ns ? sg.ring_start + v : sg.child_lo + 3 * p + v;
+                        read.insert(key(sg.child, x, y));
                     }
             }
         }
         for (long long w : written)
             if (read.count(w)) { h->r_two_pass = true; break; }
-        h->r_elems = first;
-        h->n_rseg = (int)segs.size();
-        stage_len = std::max(stage_len, (size_t)first);
-        if (int rc = upload(&h->d_rseg, segs)) return rc;
-        std::vector<int2> ch;
-        for (int q = 0; q < (int)segs.size(); ++q)
-            for (int o = 0; o < segs[q].count; o += 256) ch.push_back(make_int2(q, o));
-        h->n_rchunk = (int)ch.size();
-        if (int rc = upload(&h->d_rchunk, ch)) return rc;
+        auto make = [&](int k, int mode, int srank, int64_t first) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            return RSeg{sg.child, sg.parent, sg.side >= TS_SOUTH, sg.child_lo, sg.ring_start, sg.parent_line,
+                        sg.parent_lo, sg.parent_hi - sg.parent_lo, first, mode, srank};
+        };
+        auto geom = [&](int k, int &src, int &dst, int &count) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            src = sg.child; dst = sg.parent; count = sg.parent_hi - sg.parent_lo;
+        };
+        if (int rc = build_lists(h->r_send, h->r_local, h->r_recv, make, d->n_restrict, geom, h->r_two_pass, 1))
+            return rc;
     }
-    // ---- prolongation segments (coupling.py:318-340)
     {
-        std::vector<PSeg> segs;
         std::unordered_set<long long> written, read;
         auto key = [](int b, int arr, int x, int y) {
             return ((long long)b << 44) ^ ((long long)arr << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8);
         };
-        int64_t first = 0;
         for (int k = 0; k < d->n_prolong; ++k) {
-            const ts_flux_segment &s = d->prolong_segs[k];
-            if (!check_blk(s.parent) || !check_blk(s.child) || s.side < 0 || s.side > 3)
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            if (!check_blk(sg.parent) || !check_blk(sg.child) || sg.side < 0 || sg.side > 3)
                 return fail(TS_ERR_INVALID, "bad prolongation segment %d", k);
-            const int count = s.parent_hi - s.parent_lo;
-            if (count < 0 || s.child_hi - s.child_lo != 3 * count)
+            const int count = sg.parent_hi - sg.parent_lo;
+            if (count < 0 || sg.child_hi - sg.child_lo != 3 * count)
                 return fail(TS_ERR_INVALID, "prolongation segment %d: spans disagree", k);
             if (count == 0) continue;
-            const bool ns = s.side >= TS_SOUTH;
-            if (d->blocks[s.child].owner != d->blocks[s.parent].owner) h->x_prolong = true;
-            if (owned(s.parent)) {
-                segs.push_back(PSeg{s.parent, s.child, ns, s.child_lo, s.child_face_line, s.parent_face_line,
-                                    s.parent_lo, count, first});
-                first += 3 * count;
-            }
+            const bool ns = sg.side >= TS_SOUTH;
+            if (d->blocks[sg.child].owner != d->blocks[sg.parent].owner) h->x_prolong = true;
             const int arr = ns ? 2 : 1;
             for (int p = 0; p < count; ++p) {
-                read.insert(key(s.parent, arr, ns ? s.parent_lo + p : s.parent_face_line,
-                                ns ? s.parent_face_line : s.parent_lo + p));
+                read.insert(key(sg.parent, arr, ns ? sg.parent_lo + p : sg.parent_face_line,
+                                ns ? sg.parent_face_line : sg.parent_lo + p));
                 for (int u = 0; u < 3; ++u) {
-                    const int a = s.child_lo + 3 * p + u;
-                    written.insert(key(s.child, arr, ns ? a : s.child_face_line, ns ? s.child_face_line : a));
+                    const int a = sg.child_lo + 3 * p + u;
+                    written.insert(key(sg.child, arr, ns ? a : sg.child_face_line, ns ? sg.child_face_line : a));
                 }
             }
         }
         for (long long w : written)
             if (read.count(w)) { h->p_two_pass = true; break; }
-        h->p_elems = first;
-        h->n_pseg = (int)segs.size();
-        stage_len = std::max(stage_len, (size_t)first);
-        if (int rc = upload(&h->d_pseg, segs)) return rc;
-        std::vector<int2> ch;
-        for (int q = 0; q < (int)segs.size(); ++q)
-            for (int o = 0; o < 3 * segs[q].count; o += 256) ch.push_back(make_int2(q, o));
-        h->n_pchunk = (int)ch.size();
-        if (int rc = upload(&h->d_pchunk, ch)) return rc;
+        auto make = [&](int k, int mode, int srank, int64_t first) {
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            return PSeg{sg.parent, sg.child, sg.side >= TS_SOUTH, sg.child_lo, sg.child_face_line,
+                        sg.parent_face_line, sg.parent_lo, sg.parent_hi - sg.parent_lo, first, mode, srank};
+        };
+        auto geom = [&](int k, int &src, int &dst, int &count) {
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            src = sg.parent; dst = sg.child; count = sg.parent_hi - sg.parent_lo;
+        };
+        if (int rc = build_lists(h->p_send, h->p_local, h->p_recv, make, d->n_prolong, geom, h->p_two_pass, 3))
+            return rc;
     }
+    // receive-area bases: own now, peers' as their arenas are mapped
+    h->recv_base.assign(h->nranks, nullptr);
+    if (h->arena) h->recv_base[h->rank] = (double *)(h->arena + h->recv_off[h->rank]);
+    CK(cudaMalloc((void **)&h->d_recv, h->nranks * sizeof(double *)));
+    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->nranks * sizeof(double *), cudaMemcpyHostToDevice));
     if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
 
     // ---- halo strips (exchange.py:218-275) as deduplicated element copies
@@ -928,12 +984,10 @@ int ts_phase(ts_handle *h, int32_t phase)
     switch (phase) {
     case TS_PH_MASS: launch_mass(a, h->d_all, h->n_all, false, s); break;
     case TS_PH_RESTRICT:
-        if (h->r_two_pass) {
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 1, s);
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, h->d_stage, 2, s);
-        } else {
-            launch_restrict(a, h->d_rseg, h->d_rchunk, h->n_rchunk, nullptr, 0, s);
-        }
+        launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, s);
+        launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, s);
+        if (h->x_restrict) barrier(h, s);
+        launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, s);
         break;
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
     case TS_PH_MOMENTUM:
@@ -945,12 +999,10 @@ int ts_phase(ts_handle *h, int32_t phase)
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
     case TS_PH_PROLONG:
-        if (h->p_two_pass) {
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 1, s);
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, h->d_stage, 2, s);
-        } else {
-            launch_prolong(a, h->d_pseg, h->d_pchunk, h->n_pchunk, nullptr, 0, s);
-        }
+        launch_prolong(a, h->p_send.d, h->p_send.ch, h->p_send.nch, h->d_stage, s);
+        launch_prolong(a, h->p_local.d, h->p_local.ch, h->p_local.nch, h->d_stage, s);
+        if (h->x_prolong) barrier(h, s);
+        launch_prolong(a, h->p_recv.d, h->p_recv.ch, h->p_recv.nch, h->d_stage, s);
         break;
     case TS_PH_HALO_FLUX: launch_copies(a, h->d_hflux, h->n_hflux, false, s); break;
     case TS_PH_OUTPUT:
@@ -1090,10 +1142,15 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_all);
     cudaFree(h->d_perim);
     cudaFree(h->d_err_next);
-    cudaFree(h->d_rseg);
-    cudaFree(h->d_pseg);
-    cudaFree(h->d_rchunk);
-    cudaFree(h->d_pchunk);
+    for (auto *L : {&h->r_send, &h->r_local, &h->r_recv}) {
+        cudaFree(L->d);
+        cudaFree(L->ch);
+    }
+    for (auto *L : {&h->p_send, &h->p_local, &h->p_recv}) {
+        cudaFree(L->d);
+        cudaFree(L->ch);
+    }
+    cudaFree(h->d_recv);
     cudaFree(h->d_heta);
     cudaFree(h->d_hflux);
     cudaFree(h->d_edge);
@@ -1158,6 +1215,8 @@ int ts_ipc_import(ts_handle *h, int32_t peer, const void *in, int64_t len)
     CK(cudaIpcOpenMemHandle(&sig, hs, cudaIpcMemLazyEnablePeerAccess));
     h->peer_arena[peer] = (char *)arena;
     h->peer_sig[peer] = (unsigned long long *)sig;
+    h->recv_base[peer] = arena ? (double *)((char *)arena + h->recv_off[peer]) : nullptr;
+    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->nranks * sizeof(double *), cudaMemcpyHostToDevice));
     for (int k = 0; k < h->nb; ++k)
         if (h->desc[k].owner == peer) place_block(h->hb[k], (char *)arena + h->off[k], false);
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));

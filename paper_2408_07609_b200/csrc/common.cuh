@@ -33,15 +33,20 @@ struct Tile {
 };
 
 // one restriction segment (coupling.EtaSegment + its link)
+// mode 0: compute and write the parent cell; 1: compute into a buffer
+// (srank < 0: the local stage; else rank srank's receive area); 2: write the
+// parent cell from a buffer.  first = the segment's offset in that buffer.
 struct RSeg {
     int32_t child, parent, ns, a, ring, pline, pa, count;
-    int64_t first;                  // first element (parent cell) index
+    int64_t first;
+    int32_t mode, srank;
 };
 
 // one prolongation segment (coupling.FluxSegment + its link)
 struct PSeg {
     int32_t parent, child, ns, a, cline, pline, pa, count;
-    int64_t first;                  // first element (child face) index
+    int64_t first;                  // offset (child faces) in its buffer
+    int32_t mode, srank;            // as RSeg
 };
 
 // element copy: dst[dst_idx] = src[src_idx]; arr 0 eta, 1 m, 2 n (the
@@ -83,6 +88,7 @@ struct StepArgs {
     unsigned long long *err_next;   // errors of the fused next-step mass
     const int *acc_flag;            // fold previous step's outputs in K_mass
     int multi;                      // >1 rank: exchange kernels fence their peer stores
+    double *const *recv;            // [n_ranks] receive areas of the cross-rank coupling
 };
 
 // inter-GPU phase barrier (one process per GPU): every rank bumps its epoch,
@@ -105,9 +111,9 @@ bool momentum_split(int W);     // the width-W group uses per-CTA dirty flags
 int momentum_tiles_per_cta(int W);
 void launch_promote(const StepArgs &a, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
-                     int mode, cudaStream_t s);
+                     cudaStream_t s);
 void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int nchunks, double *stage,
-                    int mode, cudaStream_t s);
+                    cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
 int debug_counters(unsigned long long *out, int n);

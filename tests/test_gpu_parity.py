@@ -66,6 +66,20 @@ def test_run_parity(cuda_device, oracle_mod, product, name, nr):
     gpu.close()
 
 
+@pytest.mark.parametrize("nr", (1, 4))
+def test_cfg5_strips_parity(cuda_device, oracle_mod, product, nr):
+    """BASELINE config 5 (single 10 m level in 8 abutting strips, coast in
+    the last strip) at 1/50 scale: 400 x 400 cells, 200 steps."""
+    system, settings, n = systems.cfg5(product, 0.02)
+    plan = _plan(product, system, nr)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    gpu.run(n, threaded=False)
+    orc.run(n)
+    assert_same(gpu, orc, f"cfg5 after {n} steps")
+    gpu.close()
+
+
 @pytest.mark.parametrize("name", ("cfg1", "cfg2"))
 def test_baseline_config_parity(cuda_device, oracle_mod, product, name):
     """BASELINE configs 1 and 2 at their full step counts (1000 / 2000)."""

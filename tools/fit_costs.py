@@ -4,7 +4,7 @@ The reference fits a per-block GPU cost model from timed momentum calls
 (balance.py:301-328, fit_cost_model).  Here the march's cost depends on the
 block width (lanes per tile), so each width class is timed on its own:
 a single-level system of identical, non-touching blocks of that width
-(~8 M cells, enough to fill the GPU), mass and momentum kernel times from
+(40 M cells: many waves, so the tail of the last wave is negligible), mass and momentum kernel times from
 the library's per-step events.
 
     python tools/fit_costs.py [--widths 24,36,48,60,90]   (prints JSON)
@@ -22,7 +22,7 @@ import paper_2408_07609_b200 as P  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--widths", default="24,36,48,60,90")
-ap.add_argument("--cells", type=float, default=8e6)
+ap.add_argument("--cells", type=float, default=4e7)
 ap.add_argument("--steps", type=int, default=40)
 a = ap.parse_args()
 out = {}
