@@ -57,6 +57,7 @@ struct SegList {
 
 struct Group {
     int W = 0;
+    int T = 64;                         // march rows per tile of this group
     std::vector<Tile> tiles;
     Tile *d = nullptr;
     unsigned char *dirty = nullptr;     // per-CTA flags when momentum_split(W)
@@ -227,7 +228,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
                 st = h->side[x - 1];
                 CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
             }
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, (variant & kFuse) != 0, gr.dirty, st);
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, (variant & kFuse) != 0, gr.dirty, st);
             n += (gr.dirty && !(variant & kFuse)) ? 2 : 1;
             if (par && x > 0) {
                 CK(cudaEventRecord(h->ev_join[x - 1], st));
@@ -437,6 +438,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
     h->g = d->gravity;
     h->thr = d->wet_threshold;
     h->nb = d->n_blocks;
+    if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
+    if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
     if (d->tile_rows > 0) {
         if ((d->tile_rows + 2) % 3 != 0)
             return fail(TS_ERR_INVALID, "tile_rows + 2 must be a multiple of 3, got %d", d->tile_rows);
@@ -547,19 +550,46 @@ int create_impl(const ts_desc *d, ts_handle *h)
                 perim.push_back(Tile{b, ia, std::min(ia + 1024, i1), ja, std::min(ja + 4096, j1), 0});
     };
     for (int k = 0; k < 4; ++k) h->groups[k].W = k + 1;
+    auto width_group = [](int nj, int &W, int &w) {
+        if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
+        else { W = 4; w = 126; }
+    };
+    // rows per tile of each group: the default 64 unless the group is too
+    // small to fill the GPU several times over, then shorter tiles (a tile's
+    // march latency is proportional to its rows, and a group's last wave of
+    // long tiles would otherwise set the momentum phase's length)
+    if (d->tile_rows <= 0 && !h->fuse) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+        double rows[4] = {0, 0, 0, 0};
+        for (int b = 0; b < h->nb; ++b) {
+            if (d->blocks[b].owner != h->rank) continue;
+            int W, w;
+            width_group(d->blocks[b].nj, W, w);
+            rows[W - 1] += (double)(d->blocks[b].ni + 1) * ((d->blocks[b].nj + 1 + w - 1) / w);
+        }
+        for (auto &gr : h->groups) {
+            const double want = 3.0 * sms * 3;          // three waves of 3 CTAs per SM
+            gr.T = 16;
+            for (int T : {64, 48, 32, 24})
+                if (rows[gr.W - 1] / T / momentum_tiles_per_cta(gr.W) >= want) { gr.T = T; break; }
+        }
+    } else {
+        for (auto &gr : h->groups) gr.T = h->T;
+    }
     for (int b = 0; b < h->nb; ++b) {
         if (d->blocks[b].owner != h->rank) continue;
         const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
         int W, w;
-        if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
-        else { W = 4; w = 126; }
+        width_group(nj, W, w);
+        const int T = h->groups[W - 1].T;
         std::vector<int> cut_cols;
         for (int j0 = 0; j0 < nj + 1; j0 += w) {
             const int j1 = std::min(j0 + w, nj + 1);
             const int mj1 = j1 == nj + 1 ? nj - 1 : j1 - 1;
             if (j1 != nj + 1 && j1 - 1 >= 1 && j1 - 1 <= nj - 2) cut_cols.push_back(j1 - 1);
-            for (int i0 = 0; i0 < ni + 1; i0 += h->T)
-                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + h->T, ni + 1), j0, j1, mj1});
+            for (int i0 = 0; i0 < ni + 1; i0 += T)
+                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, mj1});
         }
         // cells the fused kernel does not advance: rows 0 and ni-1, columns
         // 0 and nj-1, and column-tile boundary columns
@@ -815,7 +845,6 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
     CK(cudaDeviceSynchronize());
-    if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
     if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
     if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
     // signal area: peers' epochs + own epoch; its IPC handle is exported
@@ -994,7 +1023,7 @@ int ts_phase(ts_handle *h, int32_t phase)
         for (int k = 0; k < 4; ++k) {
             Group &gr = h->groups[k];
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, h->T, false, gr.dirty, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, false, gr.dirty, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;

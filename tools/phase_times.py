@@ -22,7 +22,8 @@ world = int(os.environ.get("WORLD_SIZE", "1"))
 torch.cuda.set_device(local)
 if world > 1:
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-system = P.build_kochi_scaled_config(1.0)
+scale = float(os.environ.get("KOCHI_SCALE", "1.0"))
+system = P.build_kochi_scaled_config(scale)
 settings = P.kochi_settings(system)
 cells = [b.cell_count for _, b in system.all_blocks()]
 plan = P.minmax_plan(cells, world, weights=P.b200_block_weights(system)) if world > 1 else None
