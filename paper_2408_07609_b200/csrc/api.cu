@@ -60,7 +60,6 @@ struct Group {
     int T = 64;                         // march rows per tile of this group
     std::vector<Tile> tiles;
     Tile *d = nullptr;
-    unsigned char *dirty = nullptr;     // per-CTA flags when momentum_split(W)
 };
 
 }  // namespace
@@ -80,9 +79,6 @@ struct ts_handle {
     Group groups[4];                      // W = 1..4 (momentum march)
     Tile *d_all = nullptr;                // every tile (flat mass / fold kernels)
     int n_all = 0;
-    Tile *d_perim = nullptr;              // cells outside the fused-mass interiors
-    int n_perim = 0;
-    bool fuse = false;                    // fused next-step interior mass (see enqueue_step)
     // the momentum launches of the column-width groups run as parallel
     // graph branches (the small groups fill the big one's tail)
     bool mom_par = true;
@@ -114,11 +110,9 @@ struct ts_handle {
     bool edge_serial = false;
     double *d_stage = nullptr;
     unsigned long long *d_err = nullptr;
-    unsigned long long *d_err_next = nullptr;
     int *d_accflag = nullptr;
-    // step graphs per variant (bit 0: full mass pass instead of perimeter
-    // pass; bit 1: momentum fused with the next step's interior mass) and
-    // buffer parity; kept alive because exec event-node updates refer to them
+    // step graphs per buffer parity (index [kMassAll][parity]); kept alive
+    // because exec event-node updates refer to them
     cudaGraph_t graph[4][2] = {};
     cudaGraphExec_t gexec[4][2] = {};
     cudaEvent_t ev[kPhaseEvents] = {};
@@ -143,14 +137,13 @@ StepArgs args_of(const ts_handle *h, int cur)
     a.cur = cur;
     a.thr = h->thr;
     a.err = h->d_err;
-    a.err_next = h->d_err_next;
     a.acc_flag = h->d_accflag;
     a.multi = h->nranks > 1;
     a.recv = h->d_recv;
     return a;
 }
 
-enum { kMassAll = 1, kFuse = 2 };
+enum { kMassAll = 1 };      // the one step-graph variant (slot kept for the graph tables)
 
 void barrier(ts_handle *h, cudaStream_t s)
 {
@@ -166,12 +159,7 @@ void barrier(ts_handle *h, cudaStream_t s)
 
 // The step body, in the reference's phase order (runner.py:352-365).  When
 // `events` the phase boundaries are recorded (external event nodes when
-// captured into a graph).  `variant`: kMassAll runs the continuity update on
-// every cell (first step of a run call), otherwise only on the perimeter
-// cells the previous fused momentum kernel left; kFuse makes this step's
-// momentum kernel also advance the interior cells' water level of the next
-// step (never on the last step of a run call, so the state at return is
-// exactly the reference's).
+// captured into a graph).
 int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events, int *nlaunch)
 {
     const StepArgs a = args_of(h, cur);
@@ -187,13 +175,8 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
         return 0;
     };
     if (mark(0)) return TS_ERR_CUDA;
-    if (variant & kMassAll) {
-        if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
-    } else {
-        launch_promote(a, s);
-        ++n;
-        if (h->n_perim) { launch_mass(a, h->d_perim, h->n_perim, true, s); ++n; }
-    }
+    (void)variant;
+    if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
     if (mark(1)) return TS_ERR_CUDA;
     // multi-GPU phase barriers: only around phases with
     // cross-rank stores; each one orders this rank's peer stores before the
@@ -228,8 +211,8 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
                 st = h->side[x - 1];
                 CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
             }
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, (variant & kFuse) != 0, gr.dirty, st);
-            n += (gr.dirty && !(variant & kFuse)) ? 2 : 1;
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, st);
+            ++n;
             if (par && x > 0) {
                 CK(cudaEventRecord(h->ev_join[x - 1], st));
                 CK(cudaStreamWaitEvent(s, h->ev_join[x - 1], 0));
@@ -272,7 +255,7 @@ int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         if (rc) return rc;
         if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
-        if (variant == (h->fuse ? kFuse : kMassAll)) h->launches = nl;
+        h->launches = nl;
         size_t nn = 0;
         CK(cudaGraphGetNodes(g, nullptr, &nn));
         std::vector<cudaGraphNode_t> nodes(nn);
@@ -438,8 +421,6 @@ int create_impl(const ts_desc *d, ts_handle *h)
     h->g = d->gravity;
     h->thr = d->wet_threshold;
     h->nb = d->n_blocks;
-    if (const char *f = getenv("TSUNAMI_B200_FUSE")) h->fuse = f[0] == '1';
-    if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
     if (d->tile_rows > 0) {
         if ((d->tile_rows + 2) % 3 != 0)
             return fail(TS_ERR_INVALID, "tile_rows + 2 must be a multiple of 3, got %d", d->tile_rows);
@@ -535,20 +516,10 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
     CK(cudaMalloc((void **)&h->d_err, sizeof(unsigned long long)));
     CK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
-    CK(cudaMalloc((void **)&h->d_err_next, sizeof(unsigned long long)));
-    CK(cudaMemset(h->d_err_next, 0xff, sizeof(unsigned long long)));
     CK(cudaMalloc((void **)&h->d_accflag, sizeof(int)));
     CK(cudaMemset(h->d_accflag, 0, sizeof(int)));
 
-    // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1); pad = end of
-    // the fused-mass columns (interior, minus a column-tile boundary column,
-    // whose N face j1 belongs to the next column tile)
-    std::vector<Tile> perim;
-    auto add_rect = [&](int b, int i0, int i1, int j0, int j1) {
-        for (int ia = i0; ia < i1; ia += 1024)
-            for (int ja = j0; ja < j1; ja += 4096)
-                perim.push_back(Tile{b, ia, std::min(ia + 1024, i1), ja, std::min(ja + 4096, j1), 0});
-    };
+    // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1)
     for (int k = 0; k < 4; ++k) h->groups[k].W = k + 1;
     auto width_group = [](int nj, int &W, int &w) {
         if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
@@ -558,7 +529,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     // small to fill the GPU several times over, then shorter tiles (a tile's
     // march latency is proportional to its rows, and a group's last wave of
     // long tiles would otherwise set the momentum phase's length)
-    if (d->tile_rows <= 0 && !h->fuse) {
+    if (d->tile_rows <= 0) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
         double rows[4] = {0, 0, 0, 0};
@@ -583,34 +554,14 @@ int create_impl(const ts_desc *d, ts_handle *h)
         int W, w;
         width_group(nj, W, w);
         const int T = h->groups[W - 1].T;
-        std::vector<int> cut_cols;
         for (int j0 = 0; j0 < nj + 1; j0 += w) {
             const int j1 = std::min(j0 + w, nj + 1);
-            const int mj1 = j1 == nj + 1 ? nj - 1 : j1 - 1;
-            if (j1 != nj + 1 && j1 - 1 >= 1 && j1 - 1 <= nj - 2) cut_cols.push_back(j1 - 1);
             for (int i0 = 0; i0 < ni + 1; i0 += T)
-                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, mj1});
-        }
-        // cells the fused kernel does not advance: rows 0 and ni-1, columns
-        // 0 and nj-1, and column-tile boundary columns
-        if (ni <= 2 || nj <= 2) {
-            add_rect(b, 0, ni, 0, nj);
-        } else {
-            add_rect(b, 0, 1, 0, nj);
-            add_rect(b, ni - 1, ni, 0, nj);
-            add_rect(b, 1, ni - 1, 0, 1);
-            add_rect(b, 1, ni - 1, nj - 1, nj);
-            for (int cc : cut_cols) add_rect(b, 1, ni - 1, cc, cc + 1);
+                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, 0});
         }
     }
     for (auto &gr : h->groups) {
         if (int rc = upload(&gr.d, gr.tiles)) return rc;
-        if (!gr.tiles.empty() && momentum_split(gr.W)) {
-            const int tpc = momentum_tiles_per_cta(gr.W);
-            const size_t n = (gr.tiles.size() + tpc - 1) / tpc;
-            CK(cudaMalloc((void **)&gr.dirty, n));
-            CK(cudaMemset(gr.dirty, 0, n));
-        }
     }
     {
         // cell tiles of the flat kernels (mass + fold, flush): about
@@ -629,8 +580,6 @@ int create_impl(const ts_desc *d, ts_handle *h)
         }
         h->n_all = (int)all.size();
         if (int rc = upload(&h->d_all, all)) return rc;
-        h->n_perim = (int)perim.size();
-        if (int rc = upload(&h->d_perim, perim)) return rc;
     }
 
     auto owned = [&](int b) { return b >= 0 && b < h->nb && d->blocks[b].owner == h->rank; };
@@ -845,7 +794,6 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
     CK(cudaDeviceSynchronize());
-    if (h->nranks > 1) h->fuse = false;    // fused mass assumes rank-local neighbours
     if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
     // signal area: peers' epochs + own epoch; its IPC handle is exported
     CK(cudaMalloc((void **)&h->d_sig, (h->nranks + 1) * sizeof(unsigned long long)));
@@ -858,7 +806,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_peer_sig, h->peer_sig.data(), h->nranks * sizeof(unsigned long long *),
                   cudaMemcpyHostToDevice));
     cudaGraphExec_t g;
-    return get_graph(h, h->fuse ? kFuse : kMassAll, 0, &g);
+    return get_graph(h, kMassAll, 0, &g);
 }
 
 int check_error(ts_handle *h)
@@ -909,13 +857,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
         return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
                     h->rank, h->imported, h->nranks - 1);
     cudaStream_t s = h->stream;
-    // step k of this call: the first runs the full continuity pass, the
-    // others only the perimeter cells the previous (fused) momentum kernel
-    // left; every step but the last fuses the next step's interior mass
-    auto variant_of = [&](int64_t k) {
-        if (!h->fuse) return (int)kMassAll;
-        return (k == 0 ? kMassAll : 0) | (k + 1 < n_steps ? kFuse : 0);
-    };
+    auto variant_of = [](int64_t) { return (int)kMassAll; };
     // the fold flag is cleared for the very first step of the simulation
     // (no previous outputs exist yet)
     if (h->steps == 0) CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
@@ -1023,7 +965,7 @@ int ts_phase(ts_handle *h, int32_t phase)
         for (int k = 0; k < 4; ++k) {
             Group &gr = h->groups[k];
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, false, gr.dirty, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
@@ -1091,10 +1033,6 @@ int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t 
     CK(cudaStreamSynchronize(h->stream));
     return TS_OK;
 }
-
-// guard-failure counters of a -DTS_DEBUG=1 build (0 elsewhere); not in the
-// public header
-extern "C" int ts_debug_counters(unsigned long long *out, int n) { return debug_counters(out, n); }
 
 void *ts_host_alloc(int64_t bytes)
 {
@@ -1166,11 +1104,8 @@ void ts_destroy(ts_handle *h)
             if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) {
         cudaFree(gr.d);
-        cudaFree(gr.dirty);
     }
     cudaFree(h->d_all);
-    cudaFree(h->d_perim);
-    cudaFree(h->d_err_next);
     for (auto *L : {&h->r_send, &h->r_local, &h->r_recv}) {
         cudaFree(L->d);
         cudaFree(L->ch);

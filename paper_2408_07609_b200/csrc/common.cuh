@@ -25,9 +25,8 @@ struct DevBlock {
     int32_t has_nman, pad;
 };
 
-// one unit of the march kernels: rows [i0, i1) x output columns [j0, j1);
-// pad = end of the tile's fused-mass columns (interior, not a column-tile
-// boundary); also used as plain cell rectangles by the flat kernels
+// one unit of the march kernels: face rows [i0, i1) x output columns
+// [j0, j1); also used as plain cell rectangles by the flat kernels (pad unused)
 struct Tile {
     int32_t blk, i0, i1, j0, j1, pad;
 };
@@ -85,7 +84,6 @@ struct StepArgs {
     int cur;                        // "old" buffer index
     double thr;
     unsigned long long *err;
-    unsigned long long *err_next;   // errors of the fused next-step mass
     const int *acc_flag;            // fold previous step's outputs in K_mass
     int multi;                      // >1 rank: exchange kernels fence their peer stores
     double *const *recv;            // [n_ranks] receive areas of the cross-rank coupling
@@ -105,17 +103,13 @@ void launch_barrier(const BarrierArgs &b, cudaStream_t s);
 
 void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumulate, cudaStream_t s);
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
-void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, bool fuse,
-                     unsigned char *dirty, cudaStream_t s);
-bool momentum_split(int W);     // the width-W group uses per-CTA dirty flags
+void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
 int momentum_tiles_per_cta(int W);
-void launch_promote(const StepArgs &a, cudaStream_t s);
 void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
                      cudaStream_t s);
 void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int nchunks, double *stage,
                     cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
-int debug_counters(unsigned long long *out, int n);
 void launch_repitch(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols,
                     cudaStream_t s);

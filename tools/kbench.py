@@ -23,11 +23,3 @@ cells = system.cell_count
 print(json.dumps({"lib": os.environ.get("TSUNAMI_B200_LIB", "default"), "T": a.tile_rows,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("TSUNAMI_B200_")}, "mass_ms": m * 1e3,
                   "momentum_ms": k * 1e3, "step_ms": s * 1e3, "gcells": cells / s / 1e9}))
-try:
-    import ctypes
-    from paper_2408_07609_b200 import _native as N
-    buf = (ctypes.c_ulonglong * 8)()
-    if N.lib().ts_debug_counters(buf, 8) > 0:
-        print(json.dumps({"debug_counters": list(buf)}))
-except AttributeError:
-    pass
