@@ -1,0 +1,48 @@
+"""Multi-GPU parity (one process per GPU, exchanges over NVLink peer memory):
+the decomposed run equals the 1-GPU run bitwise.  Needs at least two GPUs
+(skipped otherwise); each case runs tools/mgpu_check.py under torchrun."""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _gpus():
+    try:
+        import torch
+        return torch.cuda.device_count() if torch.cuda.is_available() else 0
+    except ImportError:                                    # pragma: no cover
+        return 0
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("system,scale,steps", (("kochi", 0.001, 40), ("quad_wetdry", 0.0, 30),
+                                                 ("kochi", 0.01, 20)))
+@pytest.mark.parametrize("ranks", (2, 4))
+def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, ranks):
+    if _gpus() < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--system", system, "--steps", str(steps)]
+    if system == "kochi":
+        cmd += ["--scale", str(scale)]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    line = [ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1]
+    out = json.loads(line)
+    assert out["ranks"] == ranks
+    assert out["bitwise_equal_to_1gpu"], out["diffs"][:5]
