@@ -55,6 +55,10 @@ class RunReport:
     n_ranks: int
     ranks: list = field(default_factory=list)
 
+    def routine_seconds(self, routine: str) -> list:
+        """Per-rank seconds of one routine (report.py:37-38)."""
+        return [r.routines.get(routine, 0.0) for r in self.ranks]
+
     def routine_totals(self):
         out = {r: 0.0 for r in ROUTINES}
         for rt in self.ranks:
