@@ -18,6 +18,7 @@ from .grid import (Block, BoundaryConditions, GridLevel, GridStructureError, Ini
 from .runner import (PHASE_SEQUENCE, ROUTINES, NumericsError, RunReport, Simulation,
                      SimulationAborted, run_simulation)
 from .schedule import build_halo_schedule, build_offset_tables
+from . import report  # noqa: E402  (run outputs: rasters, timing CSVs)
 
 __version__ = "0.1.0"
 
