@@ -9,7 +9,7 @@ sm_100a CUDA kernels through the C ABI in ``include/tsunami_b200.h``.
 
 from .balance import (B200_MODEL, GPU_REFERENCE_MODEL, CostModel, DecompositionPlan, PlanError,
                       b200_block_weights, b200_phase_weights, concat_plans,
-                      phase_balanced_plan, equal_cell_plan, fit_cost_model, minmax_plan,
+                      phase_balanced_plan, AssignmentPlan, packed_plan, equal_cell_plan, fit_cost_model, minmax_plan,
                       predict_rank_cost, rank_costs)
 from .grid import (Block, BoundaryConditions, GridLevel, GridStructureError, InitialCondition,
                    NestedGridSystem, SimulationConfig, build_kochi_scaled_config,
@@ -23,7 +23,7 @@ from . import report  # noqa: E402  (run outputs: rasters, timing CSVs)
 __version__ = "0.1.0"
 
 __all__ = [
-    "B200_MODEL", "Block", "b200_block_weights", "b200_phase_weights", "phase_balanced_plan", "BoundaryConditions", "CostModel", "DecompositionPlan",
+    "B200_MODEL", "Block", "b200_block_weights", "b200_phase_weights", "phase_balanced_plan", "AssignmentPlan", "packed_plan", "BoundaryConditions", "CostModel", "DecompositionPlan",
     "GPU_REFERENCE_MODEL", "GridLevel", "GridStructureError", "InitialCondition",
     "NestedGridSystem", "NumericsError", "PHASE_SEQUENCE", "PlanError", "ROUTINES", "RunReport",
     "Simulation", "SimulationAborted", "SimulationConfig", "build_halo_schedule",

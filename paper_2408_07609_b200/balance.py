@@ -210,6 +210,95 @@ def phase_balanced_plan(system, n_ranks: int) -> DecompositionPlan:
     return DecompositionPlan(cells, tuple(seps))
 
 
+@dataclass(frozen=True)
+class AssignmentPlan:
+    """Any block -> rank assignment (not only consecutive runs): the same
+    interface as DecompositionPlan (``n_blocks``, ``n_ranks``, ``rank_of``,
+    ``blocks_of``, ``cells``); ``separators`` is None."""
+
+    cells: tuple
+    owners: tuple
+    ranks: int
+
+    def __post_init__(self):
+        if len(self.owners) != len(self.cells) or not self.cells:
+            raise PlanError("one owner per block needed")
+        if any(not 0 <= o < self.ranks for o in self.owners):
+            raise PlanError("owner outside [0, n_ranks)")
+        if len(set(self.owners)) != self.ranks:
+            raise PlanError("every rank needs at least one block")
+
+    separators = None
+
+    @property
+    def n_blocks(self) -> int:
+        return len(self.cells)
+
+    @property
+    def n_ranks(self) -> int:
+        return self.ranks
+
+    def rank_of(self, block_index: int) -> int:
+        return self.owners[block_index]
+
+    def blocks_of(self, rank: int) -> list:
+        return [k for k, o in enumerate(self.owners) if o == rank]
+
+
+def packed_plan(system, n_ranks: int, sweeps: int = 50) -> AssignmentPlan:
+    """Blocks packed onto ranks without the consecutive-run restriction:
+    longest-processing-time placement by mass + momentum cost, then single
+    moves and pairwise swaps that lower max(mass) + max(momentum) over ranks
+    (the step's two barrier-separated phases).  Cross-rank exchanges cost
+    little here (receive areas over NVLink), block granularity a lot."""
+    mass, mom = b200_phase_weights(system)
+    n = len(mass)
+    cells = tuple(b.ni * b.nj for _, b in system.all_blocks())
+    if not 1 <= n_ranks <= n:
+        raise PlanError(f"{n_ranks} ranks infeasible for {n} blocks")
+    owners = [0] * n
+    lm, lk = [0.0] * n_ranks, [0.0] * n_ranks
+    for k in sorted(range(n), key=lambda k: -(mass[k] + mom[k])):
+        r = min(range(n_ranks), key=lambda r: (lm[r] + lk[r], r))
+        owners[k] = r
+        lm[r] += mass[k]
+        lk[r] += mom[k]
+
+    def objective():
+        return max(lm) + max(lk) + 1e-3 * max(a + b for a, b in zip(lm, lk))
+
+    cur = objective()
+    for _ in range(sweeps):
+        improved = False
+        for k in range(n):
+            a = owners[k]
+            for b in range(n_ranks):
+                if b == a or (lm[a] - mass[k] <= 0.0 and sum(1 for o in owners if o == a) == 1):
+                    continue
+                lm[a] -= mass[k]; lk[a] -= mom[k]; lm[b] += mass[k]; lk[b] += mom[k]
+                j = objective()
+                if j < cur - 1e-9 and any(o == a for i, o in enumerate(owners) if i != k):
+                    owners[k], cur, improved = b, j, True
+                    break
+                lm[a] += mass[k]; lk[a] += mom[k]; lm[b] -= mass[k]; lk[b] -= mom[k]
+            a = owners[k]
+            for q in range(k + 1, n):
+                b = owners[q]
+                if b == a:
+                    continue
+                dm, dk = mass[q] - mass[k], mom[q] - mom[k]
+                lm[a] += dm; lk[a] += dk; lm[b] -= dm; lk[b] -= dk
+                j = objective()
+                if j < cur - 1e-9:
+                    owners[k], owners[q], cur, improved = b, a, j, True
+                    a = b
+                else:
+                    lm[a] -= dm; lk[a] -= dk; lm[b] += dm; lk[b] += dk
+        if not improved:
+            break
+    return AssignmentPlan(cells, tuple(owners), n_ranks)
+
+
 def b200_block_weights(system, table=None, block_overhead_ps: float = 0.0) -> list:
     """Relative B200 step cost of every block (global order), for
     ``minmax_plan(..., weights=...)``: cells x the per-cell cost of the

@@ -84,3 +84,28 @@ def test_phase_balanced_plan_beats_summed_minmax(product, nr):
     q = product.minmax_plan(cells, nr, weights=[a + b for a, b in zip(mass, mom)])
     assert p.n_ranks == nr
     assert _phase_objective(p.separators, mass, mom) <= _phase_objective(q.separators, mass, mom) + 1e-6
+
+
+@pytest.mark.parametrize("nr", (2, 4, 8))
+def test_packed_plan_valid_and_no_worse(product, nr):
+    from paper_2408_07609_b200.balance import _phase_objective
+    system, _, _ = systems.kochi(product, 1.0)
+    mass, mom = product.b200_phase_weights(system)
+    p = product.packed_plan(system, nr)
+    assert p.n_ranks == nr and p.n_blocks == system.n_blocks and p.separators is None
+    assert sorted(k for r in range(nr) for k in p.blocks_of(r)) == list(range(system.n_blocks))
+    lm = [sum(mass[k] for k in p.blocks_of(r)) for r in range(nr)]
+    lk = [sum(mom[k] for k in p.blocks_of(r)) for r in range(nr)]
+    q = product.phase_balanced_plan(system, nr)
+    assert max(lm) + max(lk) <= _phase_objective(q.separators, mass, mom) + 1e-6
+    ideal = (sum(mass) + sum(mom)) / nr
+    assert max(lm) + max(lk) < 1.02 * ideal
+
+
+def test_assignment_plan_errors(product):
+    with pytest.raises(product.PlanError):
+        product.AssignmentPlan((1, 2), (0,), 1)
+    with pytest.raises(product.PlanError):
+        product.AssignmentPlan((1, 2), (0, 2), 2)
+    with pytest.raises(product.PlanError):
+        product.AssignmentPlan((1, 2), (0, 0), 2)

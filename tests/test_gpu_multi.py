@@ -29,15 +29,18 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("system,scale,steps", (("kochi", 0.001, 40), ("quad_wetdry", 0.0, 30),
-                                                 ("kochi", 0.01, 20)))
+@pytest.mark.parametrize("system,scale,steps,plan", (("kochi", 0.001, 40, "minmax"),
+                                                      ("quad_wetdry", 0.0, 30, "minmax"),
+                                                      ("kochi", 0.01, 20, "packed"),
+                                                      ("kochi", 0.001, 40, "packed")))
 @pytest.mark.parametrize("ranks", (2, 4))
-def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, ranks):
+def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, plan, ranks):
     if _gpus() < ranks:
         pytest.skip(f"needs {ranks} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tools", "mgpu_check.py"), "--system", system, "--steps", str(steps)]
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--system", system, "--steps", str(steps),
+           "--plan", plan]
     if system == "kochi":
         cmd += ["--scale", str(scale)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)

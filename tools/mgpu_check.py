@@ -28,6 +28,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--system", default="kochi")
 ap.add_argument("--scale", type=float, default=0.001)
 ap.add_argument("--steps", type=int, default=40)
+ap.add_argument("--plan", default="minmax", choices=("minmax", "packed"))
 args = ap.parse_args()
 
 local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -39,7 +40,7 @@ if args.system == "kochi":
 else:
     system, settings, _ = systems.make(P, args.system)
 cells = [b.cell_count for _, b in system.all_blocks()]
-plan = P.minmax_plan(cells, world)
+plan = P.minmax_plan(cells, world) if args.plan == "minmax" else P.packed_plan(system, world)
 sim = P.Simulation(system, settings, plan, distributed=True)
 for chunk in (1, args.steps // 2, args.steps - 1 - args.steps // 2):
     sim.run(chunk, threaded=False)
@@ -61,7 +62,7 @@ if rank == 0:
             if not np.array_equal(v, r, equal_nan=True):
                 ok = False
                 bad.append((bid, f, float(np.nanmax(np.abs(v - r)))))
-    print(json.dumps({"system": args.system, "ranks": world, "steps": args.steps, "separators": list(plan.separators),
+    print(json.dumps({"system": args.system, "ranks": world, "steps": args.steps, "plan": args.plan, "owners": [plan.rank_of(k) for k in range(plan.n_blocks)],
                       "blocks": len(cells), "bitwise_equal_to_1gpu": ok, "diffs": bad[:5]}), flush=True)
 ok = D.first_error(None if ok else ("mismatch",))
 dist.barrier()
