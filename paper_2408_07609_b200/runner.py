@@ -258,9 +258,9 @@ class Simulation:
         if not distributed:
             rank, world = 0, 1
         if plan is None:
-            from .balance import equal_cell_plan, minmax_plan
+            from .balance import equal_cell_plan, packed_plan
             cells = [b.ni * b.nj for _, b in ordered]
-            plan = equal_cell_plan(cells, 1) if world == 1 else minmax_plan(cells, world)
+            plan = equal_cell_plan(cells, 1) if world == 1 else packed_plan(system, world)
         if plan.n_blocks != len(ordered):
             raise ValueError(f"plan covers {plan.n_blocks} blocks, system has {len(ordered)}")
         # one process per GPU: plan rank r is GPU r; a single process runs
