@@ -26,7 +26,7 @@ scale = float(os.environ.get("KOCHI_SCALE", "1.0"))
 system = P.build_kochi_scaled_config(scale)
 settings = P.kochi_settings(system)
 cells = [b.cell_count for _, b in system.all_blocks()]
-plan = P.minmax_plan(cells, world, weights=P.b200_block_weights(system)) if world > 1 else None
+plan = P.packed_plan(system, world) if world > 1 else None
 sim = P.Simulation(system, settings, plan, device=local)
 sim.run(5, threaded=False)
 out = []
