@@ -553,7 +553,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
         const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
         int W, w;
         width_group(nj, W, w);
-        const int T = tile_momentum_rows() > 0 ? tile_momentum_rows() : h->groups[W - 1].T;
+        const int T = h->groups[W - 1].T;
         for (int j0 = 0; j0 < nj + 1; j0 += w) {
             const int j1 = std::min(j0 + w, nj + 1);
             for (int i0 = 0; i0 < ni + 1; i0 += T)

@@ -105,7 +105,6 @@ void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumula
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
 void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, cudaStream_t s);
 int momentum_tiles_per_cta(int W);
-int tile_momentum_rows();       // > 0: the two-phase tile kernel is built in, with these rows per tile
 void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
                      cudaStream_t s);
 void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int nchunks, double *stage,
