@@ -11,15 +11,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--steps", type=int, default=60)
 ap.add_argument("--tile-rows", type=int, default=0)
+ap.add_argument("--warm", type=int, default=5)
 a = ap.parse_args()
 system = P.build_kochi_scaled_config(a.scale)
 settings = P.kochi_settings(system)
 sim = P.Simulation(system, settings, tile_rows=a.tile_rows)
-sim.run(5, threaded=False)
+sim.run(a.warm, threaded=False)
 sim.set_timing(True)
 sim.run(a.steps, threaded=False)
 m, k, s = sim.kernel_seconds()
 cells = system.cell_count
-print(json.dumps({"lib": os.environ.get("TSUNAMI_B200_LIB", "default"), "T": a.tile_rows,
+print(json.dumps({"lib": os.environ.get("TSUNAMI_B200_LIB", "default"), "T": a.tile_rows, "warm": a.warm,
                   "env": {k: v for k, v in os.environ.items() if k.startswith("TSUNAMI_B200_")}, "mass_ms": m * 1e3,
                   "momentum_ms": k * 1e3, "step_ms": s * 1e3, "gcells": cells / s / 1e9}))
