@@ -1,7 +1,7 @@
 """Benchmark: Gcell-updates/s of the nested-grid tsunami step on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config kochi|cfg1|cfg2|cfg5] [--scale S]
+                    [--config kochi|cfg1|cfg2|cfg5|cfg5weak] [--scale S]
 
 Workload (BASELINE.json ``metric`` / configs[2]): the 5-level 810/270/90/30/10 m
 Kochi-shaped domain, 47,211,444 cells, dt 0.2 s (a 6-h simulation is 108,000
@@ -66,6 +66,11 @@ def build_workload(P, name, scale):
     if name == "cfg5":
         system, settings, _ = systems.cfg5(P, scale)
         return system, settings, f"cfg5 single-level 10 m, {system.cell_count} cells in 8 strips (BASELINE config 5)"
+    if name == "cfg5weak":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        system, settings, _ = systems.cfg5(P, scale, strips=world, rows=int(round(2500 * scale)))
+        return system, settings, (f"cfg5 weak scaling: one {system.levels[0].blocks[0].ni} x "
+                                  f"{system.levels[0].blocks[0].nj} strip per GPU (BASELINE config 5)")
     raise SystemExit(f"unknown config {name}")
 
 
@@ -263,7 +268,7 @@ def run_ours(args):
         "metric": "Gcell-updates/s", "value": cells * args.steps / t / 1e9, "unit": "Gcell/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak",
+        "scaling": "weak" if (world == 1 or args.config == "cfg5weak") else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": label, "cells": cells, "levels": len(system.levels),
                    "blocks": system.n_blocks, "dt_s": settings.dt,

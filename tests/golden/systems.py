@@ -128,27 +128,32 @@ def cfg2(T):
     return system, settings, 2000
 
 
-def cfg5(T, scale=1.0, strips=8):
+def cfg5(T, scale=1.0, strips=8, rows=None):
     """one 10 m level of n x n cells (n = 20000 at scale
     1, 400 M cells) as ``strips`` abutting x-strips; 50 m deep except the
-    last strip, a slope whose coast sits at 90 % of the width; a 0.3 m hump
-    near the coast."""
-    n = int(round(20000 * scale))
-    n -= n % strips
-    dx, width = 10.0, n * 10.0
-    ni = n // strips
+    last strip, a slope whose coast sits at 90 % of the x extent; a 0.3 m
+    hump near the coast.  ``rows``: rows per strip instead (weak scaling:
+    one 2500 x 20000 strip per GPU)."""
+    nj = int(round(20000 * scale))
+    if rows is None:
+        n = nj - nj % strips
+        nj, ni = n, n // strips
+    else:
+        ni = int(rows)
+    dx = 10.0
+    wx, wy = strips * ni * dx, nj * dx
     blocks = []
     for k in range(strips):
         o = (k * ni * dx, 0.0)
         if k < strips - 1:
-            h = np.full((ni, n), 50.0)
+            h = np.full((ni, nj), 50.0)
         else:
-            h = slope(o, ni, n, dx, 0.009 * width, -0.01)
-        blocks.append(T.Block(k + 1, o, ni, n, h, 0.025))
+            h = slope(o, ni, nj, dx, 0.009 * wx, -0.01)
+        blocks.append(T.Block(k + 1, o, ni, nj, h, 0.025))
     system = T.NestedGridSystem(levels=[T.GridLevel(1, dx, blocks)])
     settings = T.SimulationConfig(
         dt=0.2, total_duration=40.0,
-        initial=T.InitialCondition("gaussian", 0.3, 0.01 * width, (0.88 * width, 0.5 * width)))
+        initial=T.InitialCondition("gaussian", 0.3, 0.01 * max(wx, wy), (0.88 * wx, 0.5 * wy)))
     return system, settings, 200
 
 
