@@ -142,18 +142,20 @@ def cfg5(T, scale=1.0, strips=8, rows=None):
         ni = int(rows)
     dx = 10.0
     wx, wy = strips * ni * dx, nj * dx
+    x_last = (strips - 1) * ni * dx           # the last strip: 50 m deep at its start, then 1 %
     blocks = []
     for k in range(strips):
         o = (k * ni * dx, 0.0)
         if k < strips - 1:
             h = np.full((ni, nj), 50.0)
         else:
-            h = slope(o, ni, nj, dx, 0.009 * wx, -0.01)
+            h = slope(o, ni, nj, dx, 50.0 + 0.01 * x_last, -0.01)
         blocks.append(T.Block(k + 1, o, ni, nj, h, 0.025))
     system = T.NestedGridSystem(levels=[T.GridLevel(1, dx, blocks)])
+    sigma = 0.01 * max(wx, wy)
     settings = T.SimulationConfig(
         dt=0.2, total_duration=40.0,
-        initial=T.InitialCondition("gaussian", 0.3, 0.01 * max(wx, wy), (0.88 * wx, 0.5 * wy)))
+        initial=T.InitialCondition("gaussian", 0.3, sigma, (x_last + 0.5 * sigma, 0.5 * wy)))
     return system, settings, 200
 
 
