@@ -83,6 +83,7 @@ class ClockSampler:
 
     def __init__(self, device):
         self.device, self.proc, self.lines = device, None, []
+        self.window = (0.0, float("inf"))      # host-clock bounds of the timed region
 
     def __enter__(self):
         try:
@@ -98,7 +99,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -111,7 +115,10 @@ class ClockSampler:
     def summary(self):
         sm, smax, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        lo, hi = self.window
+        for ts, ln in self.lines:
+            if not lo <= ts <= hi:
+                continue
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -226,13 +233,18 @@ def run_ours(args):
     sim.run(args.warmup, threaded=False)
     sim.set_timing(True)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
+    # the sampler starts ahead (nvidia-smi needs a few hundred ms) and keeps
+    # only the samples read while the timed steps ran
     with ClockSampler(local) as clk:
+        sim.run(max(1, args.warmup), threaded=False)
+        barrier()
+        torch.cuda.synchronize()
+        w0 = time.time()
         start.record(ext)
         sim.run(args.steps, threaded=False)
         end.record(ext)
         torch.cuda.synchronize()
+        clk.mark(w0, time.time())
     barrier()
     sim.set_timing(False)
     t_local = start.elapsed_time(end) / 1e3
