@@ -111,10 +111,10 @@ struct ts_handle {
     double *d_stage = nullptr;
     unsigned long long *d_err = nullptr;
     int *d_accflag = nullptr;
-    // step graphs per buffer parity (index [kMassAll][parity]); kept alive
+    // step graphs per buffer parity; kept alive
     // because exec event-node updates refer to them
-    cudaGraph_t graph[4][2] = {};
-    cudaGraphExec_t gexec[4][2] = {};
+    cudaGraph_t graph[2] = {};
+    cudaGraphExec_t gexec[2] = {};
     cudaEvent_t ev[kPhaseEvents] = {};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     int cur = 0;
@@ -124,7 +124,7 @@ struct ts_handle {
     double mass_s = 0, mom_s = 0, step_s = 0;
     int launches = 0;
     bool timing = false;
-    cudaGraphNode_t ev_node[4][2][kPhaseEvents] = {};
+    cudaGraphNode_t ev_node[2][kPhaseEvents] = {};
     std::vector<cudaEvent_t> pool;                    // 5 per timed step
 };
 
@@ -143,7 +143,6 @@ StepArgs args_of(const ts_handle *h, int cur)
     return a;
 }
 
-enum { kMassAll = 1 };      // the one step-graph variant (slot kept for the graph tables)
 
 void barrier(ts_handle *h, cudaStream_t s)
 {
@@ -160,7 +159,7 @@ void barrier(ts_handle *h, cudaStream_t s)
 // The step body, in the reference's phase order (runner.py:352-365).  When
 // `events` the phase boundaries are recorded (external event nodes when
 // captured into a graph).
-int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events, int *nlaunch)
+int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunch)
 {
     const StepArgs a = args_of(h, cur);
     int n = 0;
@@ -175,7 +174,6 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, int variant, bool events
         return 0;
     };
     if (mark(0)) return TS_ERR_CUDA;
-    (void)variant;
     if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
     if (mark(1)) return TS_ERR_CUDA;
     // multi-GPU phase barriers: only around phases with
@@ -244,14 +242,14 @@ int enqueue_flush(ts_handle *h, cudaStream_t s, int buf)
     return TS_OK;
 }
 
-// capture (once) and return the executable graph of a step variant/parity
-int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
+// capture (once) and return the executable step graph of a buffer parity
+int get_graph(ts_handle *h, int c, cudaGraphExec_t *out)
 {
-    if (!h->gexec[variant][c]) {
+    if (!h->gexec[c]) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
         int nl = 0;
-        int rc = enqueue_step(h, h->stream, c, variant, true, &nl);
+        int rc = enqueue_step(h, h->stream, c, true, &nl);
         cudaError_t e = cudaStreamEndCapture(h->stream, &g);
         if (rc) return rc;
         if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
@@ -260,7 +258,7 @@ int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
         CK(cudaGraphGetNodes(g, nullptr, &nn));
         std::vector<cudaGraphNode_t> nodes(nn);
         CK(cudaGraphGetNodes(g, nodes.data(), &nn));
-        CK(cudaGraphInstantiate(&h->gexec[variant][c], g, 0));
+        CK(cudaGraphInstantiate(&h->gexec[c], g, 0));
         for (auto nd : nodes) {
             cudaGraphNodeType ty;
             CK(cudaGraphNodeGetType(nd, &ty));
@@ -268,11 +266,11 @@ int get_graph(ts_handle *h, int variant, int c, cudaGraphExec_t *out)
             cudaEvent_t ev;
             CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
             for (int k = 0; k < kPhaseEvents; ++k)
-                if (ev == h->ev[k]) h->ev_node[variant][c][k] = nd;
+                if (ev == h->ev[k]) h->ev_node[c][k] = nd;
         }
-        h->graph[variant][c] = g;
+        h->graph[c] = g;
     }
-    *out = h->gexec[variant][c];
+    *out = h->gexec[c];
     return TS_OK;
 }
 
@@ -806,7 +804,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_peer_sig, h->peer_sig.data(), h->nranks * sizeof(unsigned long long *),
                   cudaMemcpyHostToDevice));
     cudaGraphExec_t g;
-    return get_graph(h, kMassAll, 0, &g);
+    return get_graph(h, 0, &g);
 }
 
 int check_error(ts_handle *h)
@@ -857,7 +855,6 @@ int ts_run(ts_handle *h, int64_t n_steps)
         return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
                     h->rank, h->imported, h->nranks - 1);
     cudaStream_t s = h->stream;
-    auto variant_of = [](int64_t) { return (int)kMassAll; };
     // the fold flag is cleared for the very first step of the simulation
     // (no previous outputs exist yet)
     if (h->steps == 0) CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
@@ -865,7 +862,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
     // first step: its phase events apportion the call's device time to the
     // routines (runner.ROUTINES)
     cudaGraphExec_t g;
-    if (int rc = get_graph(h, variant_of(0), h->cur, &g)) return rc;
+    if (int rc = get_graph(h, h->cur, &g)) return rc;
     CK(cudaGraphLaunch(g, s));
     float ph[7] = {0};
     CK(cudaEventSynchronize(h->ev[kPhaseEvents - 1]));
@@ -885,15 +882,14 @@ int ts_run(ts_handle *h, int64_t n_steps)
             for (size_t k = old; k < h->pool.size(); ++k) CK(cudaEventCreate(&h->pool[k]));
         }
         for (int64_t k = 0; k < n; ++k) {
-            const int v = variant_of(done + k);
-            if (int rc = get_graph(h, v, h->cur, &g)) return rc;
+            if (int rc = get_graph(h, h->cur, &g)) return rc;
             if (h->timing)
                 for (int q = 0; q < 5; ++q)
-                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[v][h->cur][kTimed[q]], h->pool[5 * k + q]));
+                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[h->cur][kTimed[q]], h->pool[5 * k + q]));
             CK(cudaGraphLaunch(g, s));
             if (h->timing)    // leave the graph's own phase events in place
                 for (int q = 0; q < 5; ++q)
-                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[v][h->cur][kTimed[q]], h->ev[kTimed[q]]));
+                    CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node[h->cur][kTimed[q]], h->ev[kTimed[q]]));
             h->cur ^= 1;
         }
         h->steps += n;
@@ -1096,12 +1092,10 @@ void ts_destroy(ts_handle *h)
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    for (auto &gv : h->gexec)
-        for (auto &g : gv)
-            if (g) cudaGraphExecDestroy(g);
-    for (auto &gv : h->graph)
-        for (auto &g : gv)
-            if (g) cudaGraphDestroy(g);
+    for (auto &g : h->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : h->graph)
+        if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) {
         cudaFree(gr.d);
     }
