@@ -159,6 +159,102 @@ def cfg5(T, scale=1.0, strips=8, rows=None):
     return system, settings, 200
 
 
+class BumpInitial:
+    """Compact bump A * max(0, 1 - r^2/s^2)^2: only IEEE elementwise
+    arithmetic, so eta0 is the same on every host (unlike np.exp).  Duck-
+    types InitialCondition for runner.py:77-80 (``eta0(x, y)``)."""
+
+    kind = "bump"
+
+    def __init__(self, amplitude, sigma, center):
+        self.amplitude, self.sigma, self.center = float(amplitude), float(sigma), center
+
+    def eta0(self, x, y):
+        cx, cy = self.center
+        r2 = (x - cx) * (x - cx) + (y - cy) * (y - cy)
+        q = np.maximum(0.0, 1.0 - r2 / (self.sigma * self.sigma))
+        return self.amplitude * (q * q)
+
+
+def _split(rng, rect, unit, n_max):
+    """Guillotine split of a cell rect (x, y, w, h) into at most n_max
+    rects whose sides are multiples of ``unit`` (and >= unit)."""
+    rects = [rect]
+    while len(rects) < n_max and rng.random() < 0.75:
+        k = int(rng.integers(len(rects)))
+        x, y, w, h = rects[k]
+        axis = int(rng.integers(2))
+        size = (w, h)[axis]
+        if size < 2 * unit:
+            continue
+        cut = unit * int(rng.integers(1, size // unit))
+        if axis == 0:
+            rects[k:k + 1] = [(x, y, cut, h), (x + cut, y, w - cut, h)]
+        else:
+            rects[k:k + 1] = [(x, y, w, cut), (x, y + cut, w, h - cut)]
+    return rects
+
+
+def random_nested(T, seed):
+    """A random valid 2- or 3-level nested system (3:1, lattice-aligned,
+    enclosed): guillotine-split sibling blocks with ragged spans on every
+    level, children anywhere inside the parent level (touching its edge,
+    straddling parent seams, abutting each other), sloping bathymetry with
+    land and wet/dry fronts, scalar / zero / per-cell Manning, random edge
+    kinds, a compact bump.  Returns (system, settings, n_steps, n_ranks)."""
+    rng = np.random.default_rng(1000 + seed)
+    dx1 = 90.0
+    nx, ny = int(rng.integers(9, 31)), int(rng.integers(9, 31))
+    # a plane beach: depth 0 on a line through a random point (all wet in
+    # a third of the systems), slope 0.3-1.2 %, any direction
+    sl, th = rng.uniform(0.003, 0.012), rng.uniform(0.0, 2.0 * np.pi)
+    gx, gy = float(-sl * np.cos(th)), float(-sl * np.sin(th))
+    px, py = rng.uniform(0.0, nx * dx1), rng.uniform(0.0, ny * dx1)
+    d0 = float(-gx * px - gy * py + (rng.uniform(40.0, 60.0) if rng.random() < 0.33 else 0.0))
+    manning = (0.0, 0.025, 0.03)
+    bid = [0]
+
+    def blocks_of(rects, dx, unit_cells):
+        out = []
+        for (x, y, w, h) in _split(rng, rects, unit_cells, 3):
+            bid[0] += 1
+            o = (x * dx, y * dx)
+            hb = slope(o, w, h, dx, d0, gx, gy)
+            nm = manning[int(rng.integers(3))]
+            if rng.random() < 0.25:
+                nm = 0.01 + 0.03 * rng.random((w, h))
+            out.append(T.Block(bid[0], o, w, h, hb, nm))
+        return out
+
+    levels = [T.GridLevel(1, dx1, blocks_of((0, 0, nx, ny), dx1, 3))]
+    # level 2: one or two non-overlapping child rects (parent cells)
+    kids = []
+    for _ in range(int(rng.integers(1, 3))):
+        for _try in range(20):
+            pw, ph = int(rng.integers(2, max(3, nx // 2))), int(rng.integers(2, max(3, ny // 2)))
+            px, py = int(rng.integers(0, nx - pw + 1)), int(rng.integers(0, ny - ph + 1))
+            if all(px >= a + c or a >= px + pw or py >= b + d or b >= py + ph for a, b, c, d in kids):
+                kids.append((px, py, pw, ph))
+                break
+    lv2 = []
+    for (px, py, pw, ph) in kids:
+        lv2 += blocks_of((3 * px, 3 * py, 3 * pw, 3 * ph), dx1 / 3, 3)
+    levels.append(T.GridLevel(2, dx1 / 3, lv2))
+    if rng.random() < 0.5:
+        px, py, pw, ph = kids[0]                       # level-2 cells inside the first child rect
+        w, h = int(rng.integers(1, 3 * pw + 1)), int(rng.integers(1, 3 * ph + 1))
+        x, y = 3 * px + int(rng.integers(0, 3 * pw - w + 1)), 3 * py + int(rng.integers(0, 3 * ph - h + 1))
+        levels.append(T.GridLevel(3, dx1 / 9, blocks_of((3 * x, 3 * y, 3 * w, 3 * h), dx1 / 9, 3)))
+    system = T.NestedGridSystem(levels=levels)
+    kinds = ("reflective", "radiation")
+    bc = T.BoundaryConditions(**{s: kinds[int(rng.integers(2))] for s in ("west", "east", "south", "north")})
+    cx, cy = rng.uniform(0.0, nx * dx1), rng.uniform(0.0, ny * dx1)
+    settings = T.SimulationConfig(dt=0.2, boundary=bc, initial=BumpInitial(
+        rng.uniform(0.3, 1.5), rng.uniform(300.0, 1500.0), (cx, cy)))
+    n_ranks = int(rng.integers(1, 4))
+    return system, settings, 100, min(n_ranks, system.n_blocks)
+
+
 SMALL = ("beach", "two_parent", "identity3", "quad_wetdry", "chain")
 ALL = SMALL + ("kochi", "cfg1", "cfg2")
 
