@@ -1,5 +1,5 @@
 """Multi-GPU parity (one process per GPU, exchanges over NVLink peer memory):
-the decomposed run equals the 1-GPU run bitwise.  Needs at least two GPUs
+the decomposed run equals the 1-GPU run of the same plan bitwise.  Needs at least two GPUs
 (skipped otherwise); each case runs tools/mgpu_check.py under torchrun."""
 
 import json
@@ -32,7 +32,9 @@ def _free_port():
 @pytest.mark.parametrize("system,scale,steps,plan", (("kochi", 0.001, 40, "minmax"),
                                                       ("quad_wetdry", 0.0, 30, "minmax"),
                                                       ("kochi", 0.01, 20, "packed"),
-                                                      ("kochi", 0.001, 40, "packed")))
+                                                      ("kochi", 0.001, 40, "packed"),
+                                                      ("fuzz", 0.0, 60, "packed"),
+                                                      ("fuzz", 0.0, 60, "minmax")))
 @pytest.mark.parametrize("ranks", (2, 4))
 def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, plan, ranks):
     if _gpus() < ranks:
@@ -43,9 +45,12 @@ def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, plan, ranks
            "--plan", plan]
     if system == "kochi":
         cmd += ["--scale", str(scale)]
+    if system == "fuzz":                  # random nested systems, compared per system
+        cmd += ["--seeds", "48"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
-    line = [ln for ln in res.stdout.splitlines() if ln.startswith("{")][-1]
-    out = json.loads(line)
-    assert out["ranks"] == ranks
-    assert out["bitwise_equal_to_1gpu"], out["diffs"][:5]
+    lines = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert lines
+    for out in lines:                     # one line per system (fuzz: per random seed)
+        assert out["ranks"] == ranks
+        assert out["bitwise_equal_to_1gpu"], (out["system"], out["diffs"][:5])
