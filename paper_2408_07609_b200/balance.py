@@ -131,17 +131,24 @@ def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
 
 
 # Measured B200 cost per cell (ps) by block width: tools/fit_costs.py
-# (single-level systems of 40 M cells of one width, 30 steps; round-1
-# kernels).  The
-# march runs ceil((nj+3)/32) warps per tile, so widths just past a warp
+# (single-level systems of 40 M cells of one width, 40 steps; round-1
+# kernels).  The march gives a tile ceil((nj+3)/32) warps, or packs tiles of
+# nj + 3 threads into 128-thread CTAs (nj = 36), so widths just past a warp
 # multiple cost more per cell; the mass pass is per-cell memory work.
-B200_MASS_PS_BY_WIDTH = {24: 15.19, 36: 14.4, 48: 13.8, 60: 13.58, 90: 13.65}
-B200_MOMENTUM_PS_BY_WIDTH = {24: 36.88, 36: 48.72, 48: 36.77, 60: 29.53, 90: 29.6}
-B200_STEP_PS_BY_WIDTH = {24: 55.16, 36: 65.59, 48: 52.55, 60: 44.69, 90: 44.61}
+B200_MASS_PS_BY_WIDTH = {24: 15.09, 36: 14.2, 48: 13.56, 60: 13.34, 90: 13.36}
+B200_MOMENTUM_PS_BY_WIDTH = {24: 36.42, 36: 32.65, 48: 37.49, 60: 29.18, 90: 29.29}
+B200_STEP_PS_BY_WIDTH = {24: 54.63, 36: 49.33, 48: 53.05, 60: 44.1, 90: 44.0}
 
 
 def _lane_factor(nj: int) -> float:
-    lanes = 32 * ((nj + 3 + 31) // 32) if nj + 3 <= 128 else 128 * ((nj + 1 + 125) // 126)
+    """Threads the march allots per N-face column (csrc/api.cu tile groups:
+    one tile per warp multiple, or tiles packed into 128-thread CTAs)."""
+    L = nj + 3
+    if L > 128:
+        return 128 * ((nj + 1 + 125) // 126) / (nj + 1)
+    lanes = 32 * ((L + 31) // 32)
+    if (128 // L) * L / 128 > L / lanes + 0.03:
+        lanes = 128 / (128 // L)
     return lanes / (nj + 1)
 
 
@@ -166,7 +173,7 @@ def b200_phase_weights(system):
         if b.nj in B200_MOMENTUM_PS_BY_WIDTH:
             mom.append(n * B200_MOMENTUM_PS_BY_WIDTH[b.nj])
         else:
-            mom.append(n * 29.53 * _lane_factor(b.nj) / _lane_factor(60))
+            mom.append(n * B200_MOMENTUM_PS_BY_WIDTH[60] * _lane_factor(b.nj) / _lane_factor(60))
     return mass, mom
 
 

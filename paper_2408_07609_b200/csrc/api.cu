@@ -56,7 +56,8 @@ struct SegList {
 };
 
 struct Group {
-    int W = 0;
+    int W = 0;                          // warps per tile; packed groups: warps per CTA
+    int lanes = 0;                      // packed groups: threads per tile (nj + 3)
     int T = 64;                         // march rows per tile of this group
     std::vector<Tile> tiles;
     Tile *d = nullptr;
@@ -76,14 +77,16 @@ struct ts_handle {
     char *arena = nullptr;
     size_t arena_bytes = 0;
     int T = 64;                           // rows per march tile; T + 2 must be a multiple of 3
-    Group groups[4];                      // W = 1..4 (momentum march)
+    // momentum march groups: [0, 4) one tile per W = 1..4 warps; then the
+    // packed groups (tiles of nj + 3 threads side by side in a CTA)
+    std::vector<Group> groups = std::vector<Group>(4);
     Tile *d_all = nullptr;                // every tile (flat mass / fold kernels)
     int n_all = 0;
     // the momentum launches of the column-width groups run as parallel
     // graph branches (the small groups fill the big one's tail)
     bool mom_par = true;
-    cudaStream_t side[3] = {};
-    cudaEvent_t ev_fork = nullptr, ev_join[3] = {};
+    cudaStream_t side[7] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[7] = {};
     // contiguous device staging of host transfers (one 1-D copy + repitch
     // kernel instead of a row-by-row 2-D copy of narrow rows)
     double *d_io = nullptr;
@@ -193,12 +196,15 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
     {
         // largest group on the main stream, the others forked onto side
         // streams (parallel branches of the captured graph) and joined back
-        int order[4], ng = 0;
-        for (int k = 0; k < 4; ++k)
+        int order[8], ng = 0;
+        for (int k = 0; k < (int)h->groups.size() && ng < 8; ++k)
             if (!h->groups[k].tiles.empty()) order[ng++] = k;
+        auto work = [&](int k) {
+            const Group &g = h->groups[k];
+            return (double)g.tiles.size() * (g.lanes ? g.lanes : 32 * g.W);
+        };
         for (int x = 1; x < ng; ++x)
-            for (int y = x; y > 0 && h->groups[order[y]].tiles.size() * h->groups[order[y]].W >
-                                         h->groups[order[y - 1]].tiles.size() * h->groups[order[y - 1]].W; --y)
+            for (int y = x; y > 0 && work(order[y]) > work(order[y - 1]); --y)
                 std::swap(order[y], order[y - 1]);
         const bool par = h->mom_par && ng > 1;
         if (par) CK(cudaEventRecord(h->ev_fork, s));
@@ -209,7 +215,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
                 st = h->side[x - 1];
                 CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
             }
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, st);
+            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, gr.lanes, st);
             ++n;
             if (par && x > 0) {
                 CK(cudaEventRecord(h->ev_join[x - 1], st));
@@ -523,6 +529,38 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (nj + 3 <= 128) { W = (nj + 3 + 31) / 32; w = nj + 1; }
         else { W = 4; w = 126; }
     };
+    // A block of nj + 3 <= 128 columns may instead share 128-thread CTAs
+    // with tiles of its own width packed side by side (nj + 3 threads each)
+    // when that keeps more threads busy: nj = 36 packs 3 tiles into 117 of
+    // 128 threads instead of one tile into 39 of 64 (Kochi's 270 m level:
+    // momentum 1.479 -> 1.458 ms).  384-thread CTAs (1 per SM) for nj = 48
+    // (7 tiles, 93 %) and 160-thread CTAs (2 per SM, 3 tiles, 96 %) were
+    // slower: occupancy matters more than idle lanes.  TSUNAMI_B200_PACK=0
+    // disables packing.
+    bool pack = true;
+    if (const char *f = getenv("TSUNAMI_B200_PACK")) pack = atoi(f) != 0;
+    std::vector<int> gid(h->nb, -1);
+    for (int b = 0; b < h->nb; ++b) {
+        if (d->blocks[b].owner != h->rank) continue;
+        const int nj = d->blocks[b].nj, L = nj + 3;
+        int W, w;
+        width_group(nj, W, w);
+        gid[b] = W - 1;
+        if (!pack || L > 128) continue;
+        const double u_std = (double)L / (32 * W), u_pack = (double)((128 / L) * L) / 128;
+        if (u_pack <= u_std + 0.03) continue;
+        int k = 4;
+        for (; k < (int)h->groups.size(); ++k)
+            if (h->groups[k].lanes == L) break;
+        if (k == (int)h->groups.size()) {
+            if (k >= 8) continue;                        // graph branches are bounded
+            Group g;
+            g.W = 4;
+            g.lanes = L;
+            h->groups.push_back(g);
+        }
+        gid[b] = k;
+    }
     // rows per tile of each group: the default 64 unless the group is too
     // small to fill the GPU several times over, then shorter tiles (a tile's
     // march latency is proportional to its rows, and a group's last wave of
@@ -530,32 +568,35 @@ int create_impl(const ts_desc *d, ts_handle *h)
     if (d->tile_rows <= 0) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
-        double rows[4] = {0, 0, 0, 0};
+        std::vector<double> rows(h->groups.size(), 0.0);
         for (int b = 0; b < h->nb; ++b) {
-            if (d->blocks[b].owner != h->rank) continue;
+            if (gid[b] < 0) continue;
             int W, w;
             width_group(d->blocks[b].nj, W, w);
-            rows[W - 1] += (double)(d->blocks[b].ni + 1) * ((d->blocks[b].nj + 1 + w - 1) / w);
+            rows[gid[b]] += (double)(d->blocks[b].ni + 1) * ((d->blocks[b].nj + 1 + w - 1) / w);
         }
-        for (auto &gr : h->groups) {
+        for (int k = 0; k < (int)h->groups.size(); ++k) {
+            Group &gr = h->groups[k];
+            const int tpc = momentum_tiles_per_cta(gr.W, gr.lanes);
             const double want = 3.0 * sms * 3;          // three waves of 3 CTAs per SM
             gr.T = 16;
             for (int T : {64, 48, 32, 24})
-                if (rows[gr.W - 1] / T / momentum_tiles_per_cta(gr.W) >= want) { gr.T = T; break; }
+                if (rows[k] / T / tpc >= want) { gr.T = T; break; }
         }
     } else {
         for (auto &gr : h->groups) gr.T = h->T;
     }
     for (int b = 0; b < h->nb; ++b) {
-        if (d->blocks[b].owner != h->rank) continue;
+        if (gid[b] < 0) continue;
         const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
         int W, w;
         width_group(nj, W, w);
-        const int T = h->groups[W - 1].T;
+        Group &gr = h->groups[gid[b]];
+        const int T = gr.T;
         for (int j0 = 0; j0 < nj + 1; j0 += w) {
             const int j1 = std::min(j0 + w, nj + 1);
             for (int i0 = 0; i0 < ni + 1; i0 += T)
-                h->groups[W - 1].tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, 0});
+                gr.tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, 0});
         }
     }
     for (auto &gr : h->groups) {
@@ -958,10 +999,9 @@ int ts_phase(ts_handle *h, int32_t phase)
         break;
     case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
     case TS_PH_MOMENTUM:
-        for (int k = 0; k < 4; ++k) {
-            Group &gr = h->groups[k];
+        for (Group &gr : h->groups) {
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, gr.lanes, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
