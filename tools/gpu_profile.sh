@@ -12,5 +12,5 @@ timeout 300 python bench.py --impl reference --steps 2 > $O/${TAG}_ref.json 2> $
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/${TAG}_launches.csv \
     python bench.py --steps 3 --warmup 3 --no-cpu > $O/${TAG}_ncu_list.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_march|k_mass" \
-    --launch-skip 8 --launch-count 4 -o $O/${TAG}_full python bench.py --steps 2 --warmup 3 --no-cpu \
+    --launch-skip 10 --launch-count 5 -o $O/${TAG}_full python bench.py --steps 2 --warmup 3 --no-cpu \
     > $O/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"

@@ -61,7 +61,7 @@ json.dump({"source": "profiles/r01_ncu_full.json (ncu --set full, Kochi-1.0, one
            "kernel": "k_march", "bytes_per_step": traffic}, open(os.path.join(PR, "momentum_traffic.json"), "w"),
           indent=1)
 json.dump({"command": "tools/gpu_profile.sh: ncu --set full --clock-control none --import-source on "
-                      "-k regex:'k_march|k_mass' --launch-skip 8 --launch-count 4 python bench.py --steps 2 "
+                      "-k regex:'k_march|k_mass' --launch-skip 10 --launch-count 5 python bench.py --steps 2 "
                       "--warmup 3 --no-cpu", "kernels": kern},
           open(os.path.join(PR, "r01_ncu_full.json"), "w"), indent=1)
 shutil.copy(os.path.join(G, f"{tag}_bench.json"), os.path.join(PR, "r01_bench_n1.json"))
