@@ -27,9 +27,10 @@ shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(PR, "r01_launch
 with open(os.path.join(PR, "r01_launches.md"), "w") as f:
     f.write("# Round 1 launch list (Kochi-1.0, 47,211,444 cells, 1 B200)\n\n")
     f.write("`ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 3 "
-            "--warmup 3 --no-cpu` (tools/gpu_profile.sh): 9 graph steps (3 warm-up, 3 timed, 3 end-to-end) "
-            "plus the end-of-run accumulator flush of each run and the end-to-end leg's host-transfer "
-            "repitch kernels. Cold-cache, serialised per-launch times; the raw list is `r01_launches.csv`.\n\n")
+            "--warmup 3 --no-cpu` (tools/gpu_profile.sh): 12 graph steps (3 warm-up, 3 more while the "
+            "clock sampler starts, 3 timed, 3 end-to-end) plus the end-of-run accumulator flush of each "
+            "run and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch and "
+            "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group). Cold-cache, serialised per-launch times; the raw list is `r01_launches.csv`.\n\n")
     f.write("| kernel | launches | total µs | share | avg µs |\n|---|---|---|---|---|\n")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         f.write(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {v / S * 100:.1f} % | {v / cnt[k] / 1e3:.1f} |\n")
