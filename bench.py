@@ -40,6 +40,10 @@ import time
 
 import numpy as np
 
+# NCCL's own log (with NCCL_DEBUG=WARN it prints its version line on rank 0)
+# goes to stderr, so stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
