@@ -17,9 +17,9 @@ halo-eta, momentum with edge rules, prolongation, halo-flux, output maxima.
   upload of the page-locked host inputs (bathymetry with ghosts, initial
   level), K steps, download of the result maps into page-locked buffers.
 * ``roofline``: the momentum kernel (the dominant one), algorithmic bytes
-  per launch / its average duration over the timed steps (per-step CUDA
-  events inside the graph, on the launch stream), against the measured HBM
-  copy bandwidth in MEASURED_PEAKS.json.
+  per launch / its average duration over the timed steps (CUDA events
+  inside the graph on every 8th timed step, on the launch stream), against
+  the measured HBM copy bandwidth in MEASURED_PEAKS.json.
 * ``cpu_baseline``: the oracle port (oracle/, plain C + OpenMP, all host
   threads) on a bounded sample of the same workload, rank 0 only.
 

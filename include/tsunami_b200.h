@@ -164,9 +164,10 @@ int64_t ts_steps_done(ts_handle *h);
 int64_t ts_device_bytes(ts_handle *h);
 /* kernels launched per ts_run step (graph nodes) */
 int32_t ts_launches_per_step(ts_handle *h);
-/* timing mode: every graph-replayed step of ts_run records the mass,
+/* timing mode: every 8th graph-replayed step of ts_run records the mass,
  * momentum and whole-step boundaries into its own CUDA events (on the launch
- * stream); ts_kernel_seconds returns their averages */
+ * stream; rebinding a launch's event nodes costs it ~9 us, so the steps in
+ * between run untouched); ts_kernel_seconds returns their averages */
 int ts_set_timing(ts_handle *h, int32_t on);
 /* average device time (s) of the momentum kernel over the last ts_run's
  * timed graph replays, measured with events on the launch stream */
