@@ -48,6 +48,10 @@ constexpr int kPhaseEvents = 8;
 // whole step (0,7)
 constexpr int kTimed[5] = {0, 1, 3, 4, 7};
 constexpr int kTimingEvery = 8;           // timing mode: every 8th step is sampled
+#ifndef TS_STEPS_PER_GRAPH
+#define TS_STEPS_PER_GRAPH 4
+#endif
+constexpr int kStepsPerGraph = TS_STEPS_PER_GRAPH;   // ts_run launches steps in graphs of 4 (even)
 
 template <typename S>
 struct SegList {
@@ -119,6 +123,11 @@ struct ts_handle {
     // because exec event-node updates refer to them
     cudaGraph_t graph[2] = {};
     cudaGraphExec_t gexec[2] = {};
+    // kStepsPerGraph consecutive steps in one graph (starting at buffer
+    // parity c): fewer graph-launch boundaries per step
+    cudaGraph_t graph_multi[2] = {};
+    cudaGraphExec_t gexec_multi[2] = {};
+    cudaGraphNode_t ev_node_multi[2][kPhaseEvents] = {};
     cudaEvent_t ev[kPhaseEvents] = {};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     int cur = 0;
@@ -278,6 +287,39 @@ int get_graph(ts_handle *h, int c, cudaGraphExec_t *out)
         h->graph[c] = g;
     }
     *out = h->gexec[c];
+    return TS_OK;
+}
+
+// capture (once) kStepsPerGraph steps from parity c (phase events only in
+// the first, so timing samples stay one per graph)
+int get_graph_multi(ts_handle *h, int c, cudaGraphExec_t *out)
+{
+    if (!h->gexec_multi[c]) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = 0;
+        for (int k = 0; k < kStepsPerGraph && !rc; ++k)
+            rc = enqueue_step(h, h->stream, c ^ (k & 1), k == 0, nullptr);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        CK(cudaGraphInstantiate(&h->gexec_multi[c], g, 0));
+        size_t nn = 0;
+        CK(cudaGraphGetNodes(g, nullptr, &nn));
+        std::vector<cudaGraphNode_t> nodes(nn);
+        CK(cudaGraphGetNodes(g, nodes.data(), &nn));
+        for (auto nd : nodes) {
+            cudaGraphNodeType ty;
+            CK(cudaGraphNodeGetType(nd, &ty));
+            if (ty != cudaGraphNodeTypeEventRecord) continue;
+            cudaEvent_t ev;
+            CK(cudaGraphEventRecordNodeGetEvent(nd, &ev));
+            for (int k = 0; k < kPhaseEvents; ++k)
+                if (ev == h->ev[k]) h->ev_node_multi[c][k] = nd;
+        }
+        h->graph_multi[c] = g;
+    }
+    *out = h->gexec_multi[c];
     return TS_OK;
 }
 
@@ -933,11 +975,30 @@ int ts_run(ts_handle *h, int64_t n_steps)
             h->pool.resize(5 * n);
             for (size_t k = old; k < h->pool.size(); ++k) CK(cudaEventCreate(&h->pool[k]));
         }
-        // timing samples every kTimingEvery-th step: rebinding a launch's
-        // event nodes costs the step ~9 us of device time (measured), so the
-        // other steps run the graph untouched
+        // steps go out in graphs of kStepsPerGraph (single-step graphs for
+        // the remainder); timing samples the first step of every
+        // kTimingEvery-th step's graph: rebinding a launch's event nodes
+        // costs it ~9 us of device time (measured), so the other launches
+        // run their graph untouched
         int64_t ns = 0;
-        for (int64_t k = 0; k < n; ++k) {
+        for (int64_t k = 0; k < n;) {
+            if (n - k >= kStepsPerGraph) {
+                if (int rc = get_graph_multi(h, h->cur, &g)) return rc;
+                const bool sample = h->timing && k % kTimingEvery == 0;
+                if (sample)
+                    for (int q = 0; q < 5; ++q)
+                        CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node_multi[h->cur][kTimed[q]],
+                                                                h->pool[5 * ns + q]));
+                CK(cudaGraphLaunch(g, s));
+                if (sample) {
+                    for (int q = 0; q < 5; ++q)
+                        CK(cudaGraphExecEventRecordNodeSetEvent(g, h->ev_node_multi[h->cur][kTimed[q]],
+                                                                h->ev[kTimed[q]]));
+                    ++ns;
+                }
+                k += kStepsPerGraph;       // an even count: the parity is unchanged
+                continue;
+            }
             if (int rc = get_graph(h, h->cur, &g)) return rc;
             const bool sample = h->timing && k % kTimingEvery == 0;
             if (sample)
@@ -950,6 +1011,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
                 ++ns;
             }
             h->cur ^= 1;
+            ++k;
         }
         h->steps += n;
         done += n;
@@ -1150,6 +1212,10 @@ void ts_destroy(ts_handle *h)
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    for (auto &g : h->gexec_multi)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : h->graph_multi)
+        if (g) cudaGraphDestroy(g);
     for (auto &g : h->gexec)
         if (g) cudaGraphExecDestroy(g);
     for (auto &g : h->graph)
