@@ -448,16 +448,27 @@ size_t pitch_of(int nj)
     return align_up((size_t)nj + 5, 4);
 }
 
+// Ghosted arrays start TS_BASE_SHIFT doubles past a 256-byte boundary, so
+// that with the 32-byte row pitch every row's interior (column g = 2 on)
+// starts on a 32-byte sector: the kernels' interior row reads and writes
+// then cover whole sectors (no partial-sector writes for L2 to fill from
+// DRAM at the row ends).
+#ifndef TS_BASE_SHIFT
+#define TS_BASE_SHIFT 2
+#endif
+
 void place_block(DevBlock &B, char *p, bool with_nman)
 {
     const size_t P = B.P;
-    const size_t cell = (size_t)(B.ni + 4) * P, mrows = (size_t)(B.ni + 5) * P, acc = (size_t)B.ni * P;
+    const size_t cell = (size_t)(B.ni + 4) * P + TS_BASE_SHIFT, mrows = (size_t)(B.ni + 5) * P + TS_BASE_SHIFT;
+    const size_t acc = (size_t)B.ni * P;
     auto take = [&](size_t n) { double *q = (double *)p; p += align_up(n * 8, 256); return q; };
-    B.eta[0] = take(cell); B.eta[1] = take(cell);
-    B.m[0] = take(mrows); B.m[1] = take(mrows);
-    B.n[0] = take(cell); B.n[1] = take(cell);
-    B.h = take(cell);
-    double *nm = take(cell);
+    auto take_g = [&](size_t n) { return take(n) + TS_BASE_SHIFT; };
+    B.eta[0] = take_g(cell); B.eta[1] = take_g(cell);
+    B.m[0] = take_g(mrows); B.m[1] = take_g(mrows);
+    B.n[0] = take_g(cell); B.n[1] = take_g(cell);
+    B.h = take_g(cell);
+    double *nm = take_g(cell);
     B.nman = with_nman ? nm : nullptr;
     B.acc_eta = take(acc); B.acc_speed = take(acc); B.acc_inund = take(acc);
 }
@@ -505,7 +516,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (bd.owner == h->rank && (!bd.h_ext || !bd.eta0))
             return fail(TS_ERR_INVALID, "block %lld: missing h_ext/eta0", (long long)bd.block_id);
         const size_t P = pitch_of(bd.nj);
-        const size_t cell = (size_t)(bd.ni + 4) * P, mrows = (size_t)(bd.ni + 5) * P, acc = (size_t)bd.ni * P;
+        const size_t cell = (size_t)(bd.ni + 4) * P + TS_BASE_SHIFT, mrows = (size_t)(bd.ni + 5) * P + TS_BASE_SHIFT;
+        const size_t acc = (size_t)bd.ni * P;
         size_t need = 0;
         need += 2 * align_up(cell * 8, 256) + 2 * align_up(mrows * 8, 256) + 2 * align_up(cell * 8, 256);
         need += 2 * align_up(cell * 8, 256);         // h and (reserved) Manning n
