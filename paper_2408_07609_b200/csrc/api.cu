@@ -443,9 +443,12 @@ int upload(Tv **dptr, const std::vector<Tv> &v)
 // row pitch (doubles) of a block's ghosted arrays: nj + 4 columns (+1 N
 // face), rounded to 32 bytes (64- or 128-byte rows measured slower: mass
 // +9 us, prolongation +7 us per Kochi step)
+#ifndef TS_PITCH_ALIGN
+#define TS_PITCH_ALIGN 4
+#endif
 size_t pitch_of(int nj)
 {
-    return align_up((size_t)nj + 5, 4);
+    return align_up((size_t)nj + 5, TS_PITCH_ALIGN);
 }
 
 // Ghosted arrays start TS_BASE_SHIFT doubles past a 256-byte boundary, so
