@@ -40,9 +40,18 @@ import time
 
 import numpy as np
 
-# NCCL's own log (with NCCL_DEBUG=WARN it prints its version line on rank 0)
-# goes to stderr, so stdout carries exactly one JSON line
+# stdout carries exactly one JSON line: the line goes to a duplicate of the
+# original stdout, and file descriptor 1 itself is pointed at stderr, so
+# whatever native code prints there (NCCL's version line under torchrun on
+# some boxes, even with NCCL_DEBUG_FILE set) lands on stderr
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+_JSON_OUT = None
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -206,7 +215,7 @@ def run_reference(args):
                          "sample": f"{steps} steps of the full workload after 1 warm-up step"},
         "e2e": {"value": rate, "unit": "Gcell/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args):
@@ -315,7 +324,7 @@ def run_ours(args):
                                 "sample": "1 step of the full workload after 1 warm-up step "
                                           f"({dt:.1f} s)"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     sim.close()
     if dist is not None:
         dist.barrier()
@@ -323,6 +332,10 @@ def run_ours(args):
 
 
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
