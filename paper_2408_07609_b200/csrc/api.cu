@@ -582,6 +582,17 @@ int create_impl(const ts_desc *d, ts_handle *h)
             CK(cudaMemcpy2D(B.eta[k] + 2 * P + 2, P * 8, bd.eta0, (size_t)bd.nj * 8, (size_t)bd.nj * 8,
                             bd.ni, cudaMemcpyHostToDevice));
     }
+    // host-transfer staging sized once for the largest owned field, so that
+    // field uploads / downloads never reallocate (cudaFree synchronises the
+    // device and, with peers mapped, costs far more)
+    {
+        size_t io = 0;
+        for (int b = 0; b < h->nb; ++b)
+            if (d->blocks[b].owner == h->rank)
+                io = std::max(io, (size_t)(d->blocks[b].ni + 5) * (size_t)(d->blocks[b].nj + 5));
+        if (io)
+            if (int rc = io_reserve(h, io)) return rc;
+    }
     CK(cudaMalloc((void **)&h->d_blocks, sizeof(DevBlock) * h->nb));
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
     CK(cudaMalloc((void **)&h->d_err, sizeof(unsigned long long)));
