@@ -34,7 +34,7 @@ def test_reference_arm_prints_one_json_line():
 def test_native_stdout_writes_go_to_stderr():
     # what native libraries print on fd 1 (NCCL's version line) must not
     # reach stdout: simulate it with a raw write to fd 1 before the arm runs
-    code = ("import os, atexit, sys\n"
+    code = ("import os, sys\n"
             "import bench\n"
             "orig = bench.run_reference\n"
             "def noisy(args):\n"
