@@ -97,7 +97,9 @@ struct ts_handle {
     double *d_io = nullptr;
     size_t io_len = 0;
     // multi-GPU (one process per GPU): peer arenas mapped by CUDA IPC
-    unsigned long long *d_sig = nullptr;  // [0, nranks): peers' epochs; [nranks]: own epoch
+    // [0, nranks): peers' epochs; [nranks]: own epoch; [nranks + 1]: the
+    // error word (d_err), read by the peers at every phase barrier
+    unsigned long long *d_sig = nullptr;
     std::vector<char *> peer_arena;
     std::vector<unsigned long long *> peer_sig;
     unsigned long long **d_peer_sig = nullptr;
@@ -117,7 +119,7 @@ struct ts_handle {
     int64_t n_heta = 0, n_hflux = 0, n_edge = 0;
     bool edge_serial = false;
     double *d_stage = nullptr;
-    unsigned long long *d_err = nullptr;
+    unsigned long long *d_err = nullptr;  // = d_sig + nranks + 1
     int *d_accflag = nullptr;
     // step graphs per buffer parity; kept alive
     // because exec event-node updates refer to them
@@ -348,7 +350,7 @@ int field_geom(ts_handle *h, int b, int field, FieldGeom *g)
 {
     if (b < 0 || b >= h->nb) return fail(TS_ERR_INVALID, "block index %d out of range", b);
     const DevBlock &B = h->hb[b];
-    if (!B.h) return fail(TS_ERR_INVALID, "block %d is not owned by rank %d", b, h->rank);
+    if (h->desc[b].owner != h->rank) return fail(TS_ERR_INVALID, "block %d is not owned by rank %d", b, h->rank);
     const int ni = B.ni, nj = B.nj, c = h->cur;
     g->pitch = B.P;
     switch (field) {
@@ -595,7 +597,11 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     CK(cudaMalloc((void **)&h->d_blocks, sizeof(DevBlock) * h->nb));
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));
-    CK(cudaMalloc((void **)&h->d_err, sizeof(unsigned long long)));
+    // signal area: peers' epochs + own epoch + the error word (peers adopt
+    // it at every barrier); its IPC handle is exported
+    CK(cudaMalloc((void **)&h->d_sig, (h->nranks + 2) * sizeof(unsigned long long)));
+    CK(cudaMemset(h->d_sig, 0, (h->nranks + 1) * sizeof(unsigned long long)));
+    h->d_err = h->d_sig + h->nranks + 1;
     CK(cudaMemset(h->d_err, 0xff, sizeof(unsigned long long)));
     CK(cudaMalloc((void **)&h->d_accflag, sizeof(int)));
     CK(cudaMemset(h->d_accflag, 0, sizeof(int)));
@@ -913,9 +919,6 @@ int create_impl(const ts_desc *d, ts_handle *h)
     }
     CK(cudaDeviceSynchronize());
     if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
-    // signal area: peers' epochs + own epoch; its IPC handle is exported
-    CK(cudaMalloc((void **)&h->d_sig, (h->nranks + 1) * sizeof(unsigned long long)));
-    CK(cudaMemset(h->d_sig, 0, (h->nranks + 1) * sizeof(unsigned long long)));
     h->peer_arena.assign(h->nranks, nullptr);
     h->peer_sig.assign(h->nranks, nullptr);
     h->peer_arena[h->rank] = h->arena;
@@ -975,9 +978,11 @@ int ts_run(ts_handle *h, int64_t n_steps)
         return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
                     h->rank, h->imported, h->nranks - 1);
     cudaStream_t s = h->stream;
-    // the fold flag is cleared for the very first step of the simulation
-    // (no previous outputs exist yet)
-    if (h->steps == 0) CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
+    // the first step of every run folds nothing: the previous run ended with
+    // the flush (or no step ran yet), and host writes made since then must
+    // not reach the maxima (the reference folds only in a step's output
+    // phase, kernels.py:322-343)
+    CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), s));
     CK(cudaEventRecord(h->t0, s));
     // first step: its phase events apportion the call's device time to the
     // routines (runner.ROUTINES)
@@ -1264,7 +1269,6 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_edge);
     cudaFree(h->d_stage);
     cudaFree(h->d_io);
-    cudaFree(h->d_err);
     cudaFree(h->d_accflag);
     cudaFree(h->d_blocks);
     for (int p = 0; p < (int)h->peer_arena.size(); ++p)

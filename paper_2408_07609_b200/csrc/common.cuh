@@ -92,8 +92,10 @@ struct StepArgs {
 // inter-GPU phase barrier (one process per GPU): every rank bumps its epoch,
 // stores it into each peer's flag slot over NVLink and spins until every
 // peer's epoch reached its own (timeout -> error key what = 3)
+// A rank's signal area is [n_ranks] peer epochs, its own epoch, then its
+// error word: peer p's error word is peer_flags[p][n_ranks + 1].
 struct BarrierArgs {
-    unsigned long long *const *peer_flags;   // [n_ranks] peer flag arrays (own at [rank])
+    unsigned long long *const *peer_flags;   // [n_ranks] peer signal areas (own at [rank])
     unsigned long long *my_flags;            // this rank's flag array, slot per peer
     unsigned long long *epoch;
     unsigned long long *err;

@@ -57,12 +57,14 @@ def exchange_peer_handles(export_fn, import_fn, rank: int, world: int, group=Non
 
 def first_error(local, group=None):
     """The reference's first failure over ranks: the minimum of the local
-    (block order, what, i, j) keys, or None.  All ranks get the same answer."""
+    (block order, what, i, j) keys, or None.  A numerics failure ranks ahead
+    of a runtime failure (block order -1, e.g. a peer that stopped at a phase
+    barrier because of it).  All ranks get the same answer."""
     import torch.distributed as dist
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, local, group=group)
     keys = [k for k in out if k is not None]
-    return min(keys) if keys else None
+    return min(keys, key=lambda k: (k[0] < 0, k)) if keys else None
 
 
 def max_over_ranks(value: float, group=None) -> float:

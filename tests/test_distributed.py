@@ -34,6 +34,10 @@ def _worker(rank, world, port, q):
         first = D.first_error((7, 0, 0, 0) if r == 0 else (5, 2, 1, 1))
         assert first == (5, 2, 1, 1)
         assert D.first_error(None) is None
+        # a runtime failure (peer stopped at a barrier) never masks a
+        # numerics failure of another rank
+        first = D.first_error((-1, 9, 0, 0, "barrier") if r == 0 else (3, 0, 4, 4))
+        assert first == (3, 0, 4, 4)
         assert D.max_over_ranks(0.5 + r) == 0.5 + (w - 1)
         merged = D.gather_fields({10 + r: r}, root=0)
         if r == 0:
