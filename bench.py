@@ -13,13 +13,17 @@ halo-eta, momentum with edge rules, prolongation, halo-flux, output maxima.
   library's stream (CUDA events bracketing ``Simulation.run(K)``, barrier +
   synchronize on both sides, max over ranks); inputs are device resident
   and 3.8 GB > 126 MB L2, so no flush is needed.
-* ``e2e``: the same K steps through the public API with host buffers:
-  upload of the page-locked host inputs (bathymetry with ghosts, initial
-  level), K steps, download of the result maps into page-locked buffers.
+* ``e2e``: the same K steps through the public API with host buffers, as
+  a fresh run: reset of the device state, one batched upload of the
+  page-locked host inputs (bathymetry with ghosts, initial level), K steps,
+  one batched download of the result maps (max_eta, max_speed,
+  max_inundation: what the reference's run writes, cli.py:160-176) into
+  page-locked buffers.
 * ``roofline``: the momentum kernel (the dominant one), algorithmic bytes
   per launch / its average duration over the timed steps (CUDA events
   inside the graph on every 8th timed step, on the launch stream), against
-  the measured HBM copy bandwidth in MEASURED_PEAKS.json.
+  the measured HBM copy bandwidth in MEASURED_PEAKS.json; ``roofline.fp64``
+  the same kernel against the measured FP64 (DFMA) rate, its binding limit.
 * ``cpu_baseline``: the oracle port (oracle/, plain C + OpenMP, all host
   threads) on a bounded sample of the same workload, rank 0 only.
 
@@ -168,19 +172,37 @@ def profiled_traffic():
         return None
 
 
-def profiled_fp64():
-    """FP64-pipe utilisation of the widest-group march launch in the
-    committed ncu capture (the kernel is FP64-issue bound, not HBM bound)."""
+def fp64_roofline(cells, mom_s):
+    """The momentum kernel against the FP64 pipe: its FP64 instructions per
+    cell (counted by ncu, profiles/r02/march_ncu.json: sm__inst_executed_pipe_fp64
+    of every march launch of one step / cells) over the event-timed launch
+    duration, against the DFMA rate tools/micro/dp_pipe.cu measured on a
+    B200 (profiles/r02/fp64_peak.json).  The kernel is FP64/issue bound,
+    not HBM bound; this is its binding roofline."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_full.json")) as f:
-            ks = json.load(f)["kernels"]
-        k = max((k for k in ks if "march" in k["kernel"]), key=lambda k: k["gpu__time_duration.sum"])
-        return {"kernel": k["kernel"], "fp64_pipe_active_frac":
-                k["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"] / 100.0,
-                "issue_active_frac": k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100.0,
-                "source": "profiles/r01_ncu_full.json"}
-    except (OSError, ValueError, KeyError):
+        with open(os.path.join(ROOT, "profiles", "r02", "march_ncu.json")) as f:
+            prof = json.load(f)
+        with open(os.path.join(ROOT, "profiles", "r02", "fp64_peak.json")) as f:
+            peak = json.load(f)
+    except (OSError, ValueError):
         return None
+    dp_per_cell = prof["dp_thread_inst_per_cell"]
+    achieved = dp_per_cell * cells / mom_s if mom_s > 0 else None
+    return {"bound": "fp64", "unit": "DP inst/s", "achieved": achieved, "peak": peak["dp_inst_per_s"],
+            "frac": achieved / peak["dp_inst_per_s"] if achieved else None,
+            "dp_inst_per_cell": dp_per_cell, "issue_inst_per_cell": prof.get("thread_inst_per_cell"),
+            "source": "profiles/r02/march_ncu.json, profiles/r02/fp64_peak.json"}
+
+
+def workload_config(P, system, settings, label, world):
+    """The `config` dict both arms print (same workload, same plan)."""
+    counts = [b.cell_count for _, b in system.all_blocks()]
+    plan = P.packed_plan(system, world) if world > 1 else P.equal_cell_plan(counts, 1)
+    return plan, {"workload": label, "cells": system.cell_count, "levels": len(system.levels),
+                  "blocks": system.n_blocks, "dt_s": settings.dt,
+                  "parallelism": f"blocks over {world} GPU(s) (packed plan, blocks per rank "
+                                 f"{[len(plan.blocks_of(r)) for r in range(world)]})",
+                  "l2": "state 3.8 GB >> 126 MB L2; no flush"}
 
 
 def cpu_sample(system, settings, steps=2, warm=1):
@@ -203,17 +225,26 @@ def run_reference(args):
         return
     import paper_2408_07609_b200 as P
     system, settings, label = build_workload(P, args.config, args.scale)
-    steps = max(1, min(args.steps, 3))
-    warm = min(max(args.warmup, 3), 5)
+    _, config = workload_config(P, system, settings, label, args.gpus)
+    # exactly K steps after W warm-up steps, as the GPU arm, unless that
+    # would take the host more than ~4 minutes (the oracle port manages
+    # ~0.06 Gcell/s on 16-24 threads: K <= ~300 at Kochi-1.0)
+    budget_steps = max(1, int(240.0 * 0.06e9 / system.cell_count))
+    steps = max(1, min(args.steps, budget_steps))
+    warm = max(1, min(args.warmup, budget_steps // 4 + 1))
     rate, threads, dt = cpu_sample(system, settings, steps=steps, warm=warm)
     line = {
         "impl": "reference", "metric": "Gcell-updates/s", "value": rate, "unit": "Gcell/s",
         "n_gpus": args.gpus, "steps": steps, "warmup": warm, "ms_per_step": dt / steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": label, "cells": system.cell_count},
+        "higher_is_better": True,
+        "scaling": "weak" if (args.gpus == 1 or args.config == "cfg5weak") else "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "six_hour_wall_s": dt / steps * SIX_HOURS_STEPS,
         "cpu_baseline": {"value": rate, "unit": "Gcell/s", "cores": threads, "kind": "port",
-                         "sample": f"{steps} steps of the full workload after {warm} warm-up steps"},
+                         "sample": f"{steps} steps of the full workload after {warm} warm-up steps "
+                                   "(oracle/, the C restatement of the numpy reference, OpenMP over "
+                                   "blocks; the numpy reference itself is ~4x slower on the same "
+                                   "cores, SURVEY.md App. D)"},
         "e2e": {"value": rate, "unit": "Gcell/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -241,7 +272,7 @@ def run_ours(args):
     # blocks -> GPUs: packed (not only consecutive runs) so that the mass and
     # the momentum phase are both balanced under the measured B200 per-width
     # costs (balance.packed_plan)
-    plan = P.packed_plan(system, world) if world > 1 else P.equal_cell_plan(counts, 1)
+    plan, config = workload_config(P, system, settings, label, world)
     sim = P.Simulation(system, settings, plan, device=local, distributed=world > 1)
     ext = torch.cuda.ExternalStream(sim.stream_ptr, device=local)
     sim.run(args.warmup, threaded=False)
@@ -249,11 +280,15 @@ def run_ours(args):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # the sampler starts ahead (nvidia-smi needs a few hundred ms) and keeps
     # only the samples read while the timed steps ran
+    # clock samples: the second warm-up run and the timed run back to back
+    # (the same kernels under the same load; a K = 20 timed region alone is
+    # shorter than nvidia-smi's 50 ms period)
     with ClockSampler(local) as clk:
-        sim.run(max(1, args.warmup), threaded=False)
+        time.sleep(0.3)
+        w0 = time.time()
+        sim.run(max(args.warmup, 100), threaded=False)     # >= 0.2 s of load: several samples
         barrier()
         torch.cuda.synchronize()
-        w0 = time.time()
         start.record(ext)
         sim.run(args.steps, threaded=False)
         end.record(ext)
@@ -271,13 +306,16 @@ def run_ours(args):
         import pickle
         per_rank = [pickle.loads(b) for b in D.all_gather_bytes(pickle.dumps(per_rank[0]))]
 
-    # end to end through the public API with host buffers: upload the host
-    # inputs, K steps, download the result maps (every rank its own blocks)
+    # end to end through the public API with host buffers, as a fresh run:
+    # reset the device state, upload the host inputs (one batched transfer),
+    # K steps, download the result maps (one batched transfer; every rank
+    # its own blocks)
     arrays = host_block_arrays(system, settings, pinned=True)     # page-locked inputs
-    outs = sim.output_buffers(pinned=True)
+    outs = sim.output_buffers(pinned=True, fields=sim.RESULT_FIELDS)
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    sim.reset()
     h2d = sim.upload_initial_state(arrays)
     sim.run(args.steps, threaded=False)
     _, d2h = sim.download_outputs(outs)
@@ -296,11 +334,7 @@ def run_ours(args):
         "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak" if (world == 1 or args.config == "cfg5weak") else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": label, "cells": cells, "levels": len(system.levels),
-                   "blocks": system.n_blocks, "dt_s": settings.dt,
-                   "parallelism": f"blocks over {world} GPU(s) (packed plan, blocks per rank "
-                                   f"{[len(plan.blocks_of(r)) for r in range(world)]})",
-                   "l2": "state 3.8 GB >> 126 MB L2; no flush"},
+        "config": config,
         "six_hour_wall_s": t / args.steps * SIX_HOURS_STEPS,
         "step_roofline": {"bytes_per_cell_step": ALG_BYTES_STEP,
                           "achieved_gbs": ALG_BYTES_STEP * cells / (t / args.steps) / 1e9,
@@ -310,7 +344,7 @@ def run_ours(args):
                      "traffic": traffic, "alg_bytes_per_launch": ALG_BYTES_MOM * my_cells,
                      "avg_launch_s": mom_s, "peak_source": peak_src,
                      "mass_kernel_s": mass_s, "step_s_events": step_s, "rank": rank,
-                     "fp64": profiled_fp64()},
+                     "fp64": fp64_roofline(my_cells, mom_s)},
         "e2e": {"value": cells * args.steps / te / 1e9, "unit": "Gcell/s",
                 "h2d_bytes_per_step": h2d / args.steps, "d2h_bytes_per_step": d2h / args.steps,
                 "wall_s": te},
@@ -320,9 +354,10 @@ def run_ours(args):
         "clocks": clk.summary(),
     }
     if rank == 0 and not args.no_cpu and world == 1:
-        rate, threads, dt = cpu_sample(system, settings, steps=1, warm=1)
+        n_cpu = max(1, int(12.0 * 0.06e9 / cells))             # ~10-15 s of host work
+        rate, threads, dt = cpu_sample(system, settings, steps=n_cpu, warm=1)
         line["cpu_baseline"] = {"value": rate, "unit": "Gcell/s", "cores": threads, "kind": "port",
-                                "sample": "1 step of the full workload after 1 warm-up step "
+                                "sample": f"{n_cpu} steps of the full workload after 1 warm-up step "
                                           f"({dt:.1f} s)"}
     if rank == 0:
         emit(line)

@@ -153,6 +153,22 @@ int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, i
 /* BlockState.set_initial_eta (kernels.py:97-101): the ni*nj interior
  * initial level into both water-level buffers */
 int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t len);
+/* A fresh start on the same system, as constructing a new Simulation does
+ * (runner.py:59-102; BlockState and OutputAccumulators start at zero,
+ * kernels.py:39-62, 309-320): zero every owned block's water levels (both
+ * buffers, ghosts included), fluxes and running maxima, clear the error
+ * and the step count.  Bathymetry and Manning n are kept. */
+int ts_reset(ts_handle *h);
+/* Batched host->device copy of the setup inputs of n owned blocks: h_ext
+ * ((ni+4)*(nj+4), as ts_set_field(TS_H_EXT)) and the interior initial
+ * level (ni*nj, as ts_set_initial_eta) — one synchronisation for all */
+int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const double *const *h_ext,
+                     const double *const *eta0);
+/* Batched device->host copy of nf fields of n owned blocks in the
+ * reference layout (as ts_get_field): out[k * nf + f] receives field
+ * fields[f] of block blocks[k] — one synchronisation for all */
+int ts_download_fields(ts_handle *h, int32_t n, const int32_t *blocks, int32_t nf, const int32_t *fields,
+                       double *const *out);
 /* the first non-finite value of the failing step (kernels.py:115-120):
  * what = 0 water level, 1 x-flux, 2 y-flux; (i, j) local cell */
 int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j);

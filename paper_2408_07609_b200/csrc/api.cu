@@ -96,6 +96,12 @@ struct ts_handle {
     // kernel instead of a row-by-row 2-D copy of narrow rows)
     double *d_io = nullptr;
     size_t io_len = 0;
+    // batched transfers: one contiguous staging area for all owned blocks'
+    // fields of a batch, and the repitch job list
+    double *d_bulk = nullptr;
+    size_t bulk_len = 0;
+    Repitch *d_jobs = nullptr;
+    size_t jobs_len = 0;
     // multi-GPU (one process per GPU): peer arenas mapped by CUDA IPC
     // [0, nranks): peers' epochs; [nranks]: own epoch; [nranks + 1]: the
     // error word (d_err), read by the peers at every phase barrier
@@ -1193,6 +1199,130 @@ void ts_host_free(void *p)
     if (p) cudaFreeHost(p);
 }
 
+namespace {
+
+int bulk_reserve(ts_handle *h, size_t elems, size_t njobs)
+{
+    if (elems > h->bulk_len) {
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->d_bulk) CK(cudaFree(h->d_bulk));
+        h->d_bulk = nullptr;
+        h->bulk_len = 0;
+        CK(cudaMalloc((void **)&h->d_bulk, elems * 8));
+        h->bulk_len = elems;
+    }
+    if (njobs > h->jobs_len) {
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->d_jobs) CK(cudaFree(h->d_jobs));
+        h->d_jobs = nullptr;
+        h->jobs_len = 0;
+        CK(cudaMalloc((void **)&h->d_jobs, njobs * sizeof(Repitch)));
+        h->jobs_len = njobs;
+    }
+    return TS_OK;
+}
+
+int run_jobs(ts_handle *h, const std::vector<Repitch> &jobs)
+{
+    if (jobs.empty()) return TS_OK;
+    int64_t mx = 0;
+    for (auto &j : jobs) mx = std::max(mx, j.rows * j.cols);
+    CK(cudaMemcpyAsync(h->d_jobs, jobs.data(), jobs.size() * sizeof(Repitch), cudaMemcpyHostToDevice, h->stream));
+    launch_repitch_batch(h->d_jobs, (int)jobs.size(), mx, h->stream);
+    CK(cudaGetLastError());
+    return TS_OK;
+}
+
+}  // namespace
+
+int ts_reset(ts_handle *h)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    CK(cudaSetDevice(h->device));
+    for (int b = 0; b < h->nb; ++b) {
+        if (h->desc[b].owner != h->rank) continue;
+        const DevBlock &B = h->hb[b];
+        const size_t P = B.P, cell = (size_t)(B.ni + 4) * P, mrows = (size_t)(B.ni + 5) * P;
+        const size_t acc = (size_t)B.ni * P;
+        for (int k = 0; k < 2; ++k) {
+            CK(cudaMemsetAsync(B.eta[k], 0, cell * 8, h->stream));
+            CK(cudaMemsetAsync(B.m[k], 0, mrows * 8, h->stream));
+            CK(cudaMemsetAsync(B.n[k], 0, cell * 8, h->stream));
+        }
+        for (double *a : {B.acc_eta, B.acc_speed, B.acc_inund}) CK(cudaMemsetAsync(a, 0, acc * 8, h->stream));
+    }
+    CK(cudaMemsetAsync(h->d_err, 0xff, sizeof(unsigned long long), h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->cur = 0;
+    h->steps = 0;
+    return TS_OK;
+}
+
+int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const double *const *h_ext,
+                     const double *const *eta0)
+{
+    if (!h || n < 0 || (n && (!blocks || !h_ext || !eta0))) return fail(TS_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    size_t total = 0;
+    for (int k = 0; k < n; ++k) {
+        FieldGeom g;
+        if (int rc = field_geom(h, blocks[k], TS_H_EXT, &g)) return rc;
+        if (!h_ext[k] || !eta0[k]) return fail(TS_ERR_INVALID, "block %d: null input", blocks[k]);
+        const DevBlock &B = h->hb[blocks[k]];
+        total += (size_t)g.rows * g.cols + (size_t)B.ni * B.nj;
+    }
+    if (int rc = bulk_reserve(h, total, 3 * (size_t)n)) return rc;
+    std::vector<Repitch> jobs;
+    size_t off = 0;
+    for (int k = 0; k < n; ++k) {
+        const DevBlock &B = h->hb[blocks[k]];
+        const size_t he = (size_t)(B.ni + 4) * (B.nj + 4), ee = (size_t)B.ni * B.nj;
+        double *sh = h->d_bulk + off, *se = sh + he;
+        CK(cudaMemcpyAsync(sh, h_ext[k], he * 8, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemcpyAsync(se, eta0[k], ee * 8, cudaMemcpyHostToDevice, h->stream));
+        jobs.push_back(Repitch{B.h, sh, B.P, B.nj + 4, B.ni + 4, B.nj + 4});
+        // set_initial_eta: the interior of both water-level buffers
+        for (int q = 0; q < 2; ++q)
+            jobs.push_back(Repitch{B.eta[q] + 2 * (size_t)B.P + 2, se, B.P, B.nj, B.ni, B.nj});
+        off += he + ee;
+    }
+    if (int rc = run_jobs(h, jobs)) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    return TS_OK;
+}
+
+int ts_download_fields(ts_handle *h, int32_t n, const int32_t *blocks, int32_t nf, const int32_t *fields,
+                       double *const *out)
+{
+    if (!h || n < 0 || nf < 0 || (n && nf && (!blocks || !fields || !out)))
+        return fail(TS_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    std::vector<FieldGeom> geo((size_t)n * nf);
+    size_t total = 0;
+    for (int k = 0; k < n; ++k)
+        for (int f = 0; f < nf; ++f) {
+            FieldGeom &g = geo[(size_t)k * nf + f];
+            if (int rc = field_geom(h, blocks[k], fields[f], &g)) return rc;
+            if (!out[(size_t)k * nf + f]) return fail(TS_ERR_INVALID, "null output buffer");
+            total += (size_t)g.rows * g.cols;
+        }
+    if (int rc = bulk_reserve(h, total, geo.size())) return rc;
+    std::vector<Repitch> jobs;
+    std::vector<size_t> offs;
+    size_t off = 0;
+    for (auto &g : geo) {
+        jobs.push_back(Repitch{h->d_bulk + off, g.ptr, g.cols, g.pitch, g.rows, g.cols});
+        offs.push_back(off);
+        off += (size_t)g.rows * g.cols;
+    }
+    if (int rc = run_jobs(h, jobs)) return rc;
+    for (size_t q = 0; q < geo.size(); ++q)
+        CK(cudaMemcpyAsync(out[q], h->d_bulk + offs[q], (size_t)geo[q].rows * geo[q].cols * 8,
+                           cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return TS_OK;
+}
+
 int ts_error_info(ts_handle *h, int32_t *block, int32_t *what, int64_t *i, int64_t *j)
 {
     if (!h) return fail(TS_ERR_INVALID, "null handle");
@@ -1269,6 +1399,8 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_edge);
     cudaFree(h->d_stage);
     cudaFree(h->d_io);
+    cudaFree(h->d_bulk);
+    cudaFree(h->d_jobs);
     cudaFree(h->d_accflag);
     cudaFree(h->d_blocks);
     for (int p = 0; p < (int)h->peer_arena.size(); ++p)

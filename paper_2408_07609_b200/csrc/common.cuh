@@ -117,3 +117,10 @@ void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cud
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
 void launch_repitch(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols,
                     cudaStream_t s);
+// many pitched <-> contiguous copies in one launch (batched host transfers)
+struct Repitch {
+    double *dst;
+    const double *src;
+    int64_t dpitch, spitch, rows, cols;
+};
+void launch_repitch_batch(const Repitch *jobs, int njobs, int64_t max_elems, cudaStream_t s);

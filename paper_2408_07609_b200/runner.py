@@ -510,46 +510,76 @@ class Simulation:
         N.check(N.lib().ts_stream(self._h, ctypes.byref(p)))
         return int(p.value or 0)
 
+    def reset(self):
+        """A fresh start on the device (as constructing a new Simulation:
+        runner.py:59-102): water levels, fluxes and running maxima of the
+        owned blocks zeroed, step count 0.  Follow with
+        ``upload_initial_state`` to load the initial level."""
+        self._sync_in()
+        N.check(N.lib().ts_reset(self._h))
+        self._invalidate()
+        self.steps_done = 0
+        self._wet_role = "new"
+
     def upload_initial_state(self, arrays=None):
         """Copy the host inputs (ghosted bathymetry, initial level) of the
         owned blocks into the device state again — the host->device leg of an
         end-to-end run (BlockState construction + set_initial_eta,
-        kernels.py:39-62, 97-101).  ``arrays`` as returned by
-        ``host_block_arrays`` (page-locked with ``pinned=True``).  Returns the
-        bytes copied."""
+        kernels.py:39-62, 97-101) — in one batched transfer.  ``arrays`` as
+        returned by ``host_block_arrays`` (page-locked with ``pinned=True``).
+        Returns the bytes copied."""
         if arrays is None:
             arrays = host_block_arrays(self.system, self.settings)
-        L, nbytes = N.lib(), 0
-        for bid, st in self.states.items():
-            h, _, eta0 = arrays[bid]
-            st._invalidate()
-            N.check(L.ts_set_field(self._h, st._index, N.FIELDS["h_ext"], h.ctypes.data, h.size))
-            N.check(L.ts_set_initial_eta(self._h, st._index, eta0.ctypes.data, eta0.size))
-            nbytes += h.nbytes + eta0.nbytes
-        return nbytes
+        self._sync_in()
+        items = sorted(self.states.items(), key=lambda kv: kv[1]._index)
+        n = len(items)
+        idx = (ctypes.c_int32 * max(1, n))(*[st._index for _, st in items])
+        hs = [np.ascontiguousarray(arrays[bid][0], dtype=float) for bid, _ in items]
+        es = [np.ascontiguousarray(arrays[bid][2], dtype=float) for bid, _ in items]
+        hp = (ctypes.c_void_p * max(1, n))(*[a.ctypes.data for a in hs])
+        ep = (ctypes.c_void_p * max(1, n))(*[a.ctypes.data for a in es])
+        N.check(N.lib().ts_upload_inputs(self._h, n, idx, hp, ep))
+        self._invalidate()
+        return sum(a.nbytes for a in hs) + sum(a.nbytes for a in es)
 
-    def output_buffers(self, pinned: bool = False):
-        """Host buffers for ``download_outputs``: per owned block id
-        (max_eta, max_speed, max_inundation, eta_old), reference shapes."""
+    # the run's results (the rasters the reference's run writes, cli.py:160-176)
+    RESULT_FIELDS = ("max_eta", "max_speed", "max_inundation")
+    OUTPUT_FIELDS = RESULT_FIELDS + ("eta_old",)
+
+    def output_buffers(self, pinned: bool = False, fields=OUTPUT_FIELDS):
+        """Host buffers for ``download_outputs``: per owned block id one
+        array per field (default max_eta, max_speed, max_inundation,
+        eta_old), reference shapes."""
         alloc = N.pinned_empty if pinned else np.empty
-        return {bid: (alloc((st.ni, st.nj)), alloc((st.ni, st.nj)), alloc((st.ni, st.nj)),
-                      alloc((st.ni + 4, st.nj + 4)))
-                for bid, st in self.states.items()}
 
-    def download_outputs(self, out=None):
-        """Device->host read of the results of the owned blocks: max_eta,
-        max_speed, max_inundation and the current water level.  Fills
-        ``out`` (from ``output_buffers``) when given.  Returns (dict, bytes)."""
+        def shape(st, f):
+            return (st.ni, st.nj) if f.startswith("max") else st._shape(f)
+
+        return {bid: tuple(alloc(shape(st, f)) for f in fields) for bid, st in self.states.items()}
+
+    def download_outputs(self, out=None, fields=None):
+        """Device->host read of the results of the owned blocks (by default
+        max_eta, max_speed, max_inundation and the current water level; the
+        fields are inferred from the buffers' count) in one batched
+        transfer.  Fills ``out`` (from ``output_buffers``) when given.
+        Returns (dict, bytes)."""
         if out is None:
             out = self.output_buffers()
-        L, nbytes = N.lib(), 0
         self._sync_in()
-        for bid, bufs in out.items():
-            st = self.states[bid]
-            for f, a in zip(("max_eta", "max_speed", "max_inundation", "eta_old"), bufs):
-                N.check(L.ts_get_field(self._h, st._index, N.FIELDS[f], a.ctypes.data, a.size))
-                nbytes += a.nbytes
-        return out, nbytes
+        items = [(bid, self.states[bid]) for bid in out]
+        if fields is None:
+            k = len(next(iter(out.values()))) if out else 0
+            fields = self.RESULT_FIELDS if k == len(self.RESULT_FIELDS) else self.OUTPUT_FIELDS
+        n, nf = len(items), len(fields)
+        idx = (ctypes.c_int32 * max(1, n))(*[st._index for _, st in items])
+        fld = (ctypes.c_int32 * nf)(*[N.FIELDS[f] for f in fields])
+        bufs = [a for bid, _ in items for a in out[bid]]
+        for a in bufs:
+            if not (a.flags.c_contiguous and a.dtype == np.float64):
+                raise ValueError("output buffers must be C-contiguous float64 (use output_buffers)")
+        ptr = (ctypes.c_void_p * max(1, len(bufs)))(*[a.ctypes.data for a in bufs])
+        N.check(N.lib().ts_download_fields(self._h, n, idx, nf, fld, ptr))
+        return out, sum(a.nbytes for a in bufs)
 
     @property
     def device_bytes(self) -> int:

@@ -153,14 +153,17 @@ def test_message_trace(cuda_device, product, tmp_path):
 
 
 def test_end_to_end_host_buffers_match_fresh_run(cuda_device, product):
-    """The e2e leg of bench.py: upload of page-locked inputs + run + download
-    into page-locked buffers gives exactly a plain run's state."""
+    """The e2e leg of bench.py: reset of a used simulation + batched upload
+    of page-locked inputs + run + batched download into page-locked buffers
+    gives exactly a fresh simulation's state."""
     from paper_2408_07609_b200.runner import host_block_arrays
     system, settings, _ = systems.make(product, "quad_wetdry")
     plan = _plan(product, system, 1)
     fresh = product.Simulation(system, settings, plan)
     fresh.run(25, threaded=False)
     sim = product.Simulation(system, settings, plan)
+    sim.run(7, threaded=False)                 # a used state: fluxes, maxima, step count
+    sim.reset()
     arrays = host_block_arrays(system, settings, pinned=True)
     nbytes = sim.upload_initial_state(arrays)
     assert nbytes == sum(a[0].nbytes + a[2].nbytes for a in arrays.values())
@@ -174,3 +177,5 @@ def test_end_to_end_host_buffers_match_fresh_run(cuda_device, product):
         assert np.array_equal(ms, acc.max_speed)
         assert np.array_equal(mi, acc.max_inundation)
         assert np.array_equal(eo, fresh.states[bid].eta_old)
+        for f in ("eta_new", "m_old", "m_new", "n_old", "n_new"):
+            assert np.array_equal(getattr(sim.states[bid], f), getattr(fresh.states[bid], f)), f
