@@ -149,6 +149,55 @@ def host_block_arrays(system, settings, pinned: bool = False):
 
 # ------------------------------------------------------------ state views
 
+def build_descriptor(system, settings, owner, halo, tables, domain_edges_by_rank, rank=0, world=1, device=0,
+                     tile_rows=0):
+    """The ts_desc of a configured system (include/tsunami_b200.h; the body
+    of Simulation.__init__, runner.py:59-102): per-block arrays from
+    host_block_arrays, the halo entries in the reference's apply order, the
+    restriction/prolongation segments and the domain-edge rules.  Accepts the
+    reference's own objects (duck-typed).  Returns (desc, keepalive)."""
+    ordered = system.all_blocks()
+    arrays = host_block_arrays(system, settings)
+    keep = []
+    blocks = (N.BlockDesc * len(ordered))()
+    for k, (lvl, b) in enumerate(ordered):
+        h, nman, eta0 = arrays[b.block_id]
+        keep += [h, nman, eta0]
+        d = blocks[k]
+        d.block_id, d.ni, d.nj, d.owner = b.block_id, b.ni, b.nj, owner[k]
+        d.level = system.levels.index(lvl)
+        d.dx = lvl.dx
+        d.manning = float(b.manning_n) if nman is None else 0.0
+        d.h_ext = h.ctypes.data_as(N.PD)
+        d.nman_ext = nman.ctypes.data_as(N.PD) if nman is not None else None
+        d.eta0 = eta0.ctypes.data_as(N.PD)
+    idx = {b.block_id: k for k, (_, b) in enumerate(ordered)}
+    hal = [(idx[e.block_id], idx[e.peer_id], SIDE_CODE[e.side], *e.send_span, *e.recv_span)
+           for e in halo_apply_order(halo)]
+    eta_segs, flux_segs = intergrid_segments(tables)
+    rseg = [(idx[p], idx[c], SIDE_CODE[sg.side], *sg.child_span, sg.ring_start, sg.parent_line, *sg.parent_span)
+            for (p, c, sg) in eta_segs]
+    pseg = [(idx[p], idx[c], SIDE_CODE[sg.side], *sg.child_span, sg.child_face_line, sg.parent_face_line,
+             *sg.parent_span) for (p, c, sg) in flux_segs]
+    edges = [(idx[bid], SIDE_CODE[side], KIND_CODE[kind], iv[0], iv[1])
+             for r in sorted(domain_edges_by_rank) for (bid, side, iv, kind) in domain_edges_by_rank[r]]
+    desc = N.Desc()
+    desc.abi_version = N.ABI_VERSION
+    desc.n_blocks = len(ordered)
+    desc.blocks = blocks
+    desc.dt, desc.gravity = float(settings.dt), float(settings.g)
+    desc.wet_threshold = float(settings.wet_threshold)
+    for name, rows, cls in (("halo", hal, N.HaloEntryC), ("restrict_segs", rseg, N.EtaSegmentC),
+                            ("prolong_segs", pseg, N.FluxSegmentC), ("edges", edges, N.EdgeC)):
+        arr = (cls * max(1, len(rows)))(*[cls(*r) for r in rows])
+        keep.append(arr)
+        setattr(desc, name, arr)
+    desc.n_halo, desc.n_restrict, desc.n_prolong, desc.n_edges = len(hal), len(rseg), len(pseg), len(edges)
+    desc.rank, desc.n_ranks, desc.device, desc.tile_rows = rank, world, device, tile_rows
+    keep.append(blocks)
+    return desc, keep
+
+
 class DeviceBlockState:
     """BlockState-shaped view of one device-resident block (kernels.py:31-105).
 
@@ -295,50 +344,14 @@ class Simulation:
 
     # -- C ABI descriptor -------------------------------------------------
     def _create(self, ordered, tile_rows):
-        L = N.lib()
-        arrays = host_block_arrays(self.system, self.settings)
-        keep = []
-        blocks = (N.BlockDesc * len(ordered))()
-        for k, (lvl, b) in enumerate(ordered):
-            h, nman, eta0 = arrays[b.block_id]
-            keep += [h, nman, eta0]
-            d = blocks[k]
-            d.block_id, d.ni, d.nj, d.owner = b.block_id, b.ni, b.nj, self.owner[k]
-            d.level = self.system.levels.index(lvl)
-            d.dx = lvl.dx
-            d.manning = float(b.manning_n) if nman is None else 0.0
-            d.h_ext = h.ctypes.data_as(N.PD)
-            d.nman_ext = nman.ctypes.data_as(N.PD) if nman is not None else None
-            d.eta0 = eta0.ctypes.data_as(N.PD)
-        idx = self.index
-        halo = [(idx[e.block_id], idx[e.peer_id], SIDE_CODE[e.side], *e.send_span, *e.recv_span)
-                for e in halo_apply_order(self.halo)]
-        eta_segs, flux_segs = intergrid_segments(self.tables)
-        rseg = [(idx[p], idx[c], SIDE_CODE[s.side], *s.child_span, s.ring_start, s.parent_line,
-                 *s.parent_span) for (p, c, s) in eta_segs]
-        pseg = [(idx[p], idx[c], SIDE_CODE[s.side], *s.child_span, s.child_face_line,
-                 s.parent_face_line, *s.parent_span) for (p, c, s) in flux_segs]
-        edges = [(idx[bid], SIDE_CODE[side], KIND_CODE[kind], iv[0], iv[1])
-                 for r in sorted(self.domain_edges) for (bid, side, iv, kind) in self.domain_edges[r]]
-        desc = N.Desc()
-        desc.abi_version = N.ABI_VERSION
-        desc.n_blocks = len(ordered)
-        desc.blocks = blocks
-        desc.dt, desc.gravity = float(self.settings.dt), float(self.settings.g)
-        desc.wet_threshold = float(self.settings.wet_threshold)
-        arrs = []
-        for name, rows, cls in (("halo", halo, N.HaloEntryC), ("restrict_segs", rseg, N.EtaSegmentC),
-                                ("prolong_segs", pseg, N.FluxSegmentC), ("edges", edges, N.EdgeC)):
-            arr = (cls * max(1, len(rows)))(*[cls(*r) for r in rows])
-            arrs.append(arr)
-            setattr(desc, name, arr)
-        desc.n_halo, desc.n_restrict, desc.n_prolong, desc.n_edges = len(halo), len(rseg), len(pseg), len(edges)
-        desc.rank, desc.n_ranks, desc.device, desc.tile_rows = self.rank, self.world, self.device, tile_rows
+        desc, keep = build_descriptor(self.system, self.settings, self.owner, self.halo, self.tables,
+                                      self.domain_edges, self.rank, self.world, self.device, tile_rows)
         hptr = ctypes.c_void_p()
-        N.check(L.ts_create(ctypes.byref(desc), ctypes.byref(hptr)))
+        N.check(N.lib().ts_create(ctypes.byref(desc), ctypes.byref(hptr)))
         self._h = hptr
-        self._descr_counts = dict(halo=len(halo), restrict=len(rseg), prolong=len(pseg), edges=len(edges))
-        del keep, arrs
+        self._descr_counts = dict(halo=desc.n_halo, restrict=desc.n_restrict, prolong=desc.n_prolong,
+                                  edges=desc.n_edges)
+        del keep
 
     def _ipc_export(self) -> bytes:
         buf = (ctypes.c_char * 256)()

@@ -25,6 +25,17 @@ def _plan(P, system, nr):
     return P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], nr)
 
 
+def _same_bits(a, b):
+    """Elementwise identical IEEE bit patterns (so -0.0 != +0.0); any NaN
+    equals any NaN (payloads of a failed step are not compared)."""
+    a, b = np.ascontiguousarray(a, dtype=np.float64), np.ascontiguousarray(b, dtype=np.float64)
+    return (a.view(np.uint64) == b.view(np.uint64)) | (np.isnan(a) & np.isnan(b))
+
+
+def bits_equal(a, b):
+    return np.shape(a) == np.shape(b) and bool(np.all(_same_bits(a, b)))
+
+
 def assert_same(gpu, orc, where="", wet="all"):
     """``wet="interior"`` between mass and halo-eta: the reference refreshes
     ghost wet flags only when halo-eta writes the ghosts, so until then they
@@ -33,8 +44,8 @@ def assert_same(gpu, orc, where="", wet="all"):
         g = gpu.states[bid]
         for f in FIELDS:
             a, b = getattr(g, f), getattr(o, f)
-            if not np.array_equal(a, b, equal_nan=True):
-                bad = np.argwhere(~((a == b) | (np.isnan(a) & np.isnan(b))))
+            if not bits_equal(a, b):
+                bad = np.argwhere(~_same_bits(a, b))
                 raise AssertionError(f"{where} block {bid} {f}: {len(bad)} cells differ, first "
                                      f"{bad[0].tolist()} gpu={a[tuple(bad[0])]!r} "
                                      f"oracle={b[tuple(bad[0])]!r}")
@@ -44,7 +55,7 @@ def assert_same(gpu, orc, where="", wet="all"):
         assert np.array_equal(gw, ow), (where, bid, "wet")
         acc = gpu.accumulators[bid]
         for f in ACCS:
-            assert np.array_equal(getattr(acc, f), getattr(o, f), equal_nan=True), (where, bid, f)
+            assert bits_equal(getattr(acc, f), getattr(o, f)), (where, bid, f)
 
 
 @pytest.mark.parametrize("name", systems.SMALL + ("kochi",))
@@ -63,6 +74,21 @@ def test_run_parity(cuda_device, oracle_mod, product, name, nr):
         orc.run(chunk)
         done += chunk
         assert_same(gpu, orc, f"after {done} steps")
+    gpu.close()
+
+
+def test_cfg5_quarter_scale_window(cuda_device, oracle_mod, product):
+    """BASELINE config 5 at 1/4 of its cells (10,000 x 10,000 = 100 M cells
+    in 8 strips of 1250 x 10,000), 6 steps, bitwise."""
+    system, settings, _ = systems.cfg5(product, 0.5)
+    assert system.cell_count == 100_000_000
+    plan = _plan(product, system, 1)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    for chunk in (1, 5):
+        gpu.run(chunk, threaded=False)
+        orc.run(chunk)
+    assert_same(gpu, orc, "cfg5 quarter scale")
     gpu.close()
 
 
@@ -94,16 +120,21 @@ def test_baseline_config_parity(cuda_device, oracle_mod, product, name):
 
 
 def test_kochi_full_scale_window(cuda_device, oracle_mod, product):
-    """The 47,211,444-cell 5-level domain (BASELINE config 3): a short
-    window, bitwise, with the 4-rank plan's apply order."""
+    """The 47,211,444-cell 5-level domain (BASELINE config 3): a 103-step
+    window (SURVEY.md:313), bitwise, with the 4-rank plan's apply order;
+    compared after the first step, after 3 and at the end."""
     system, settings, _ = systems.kochi(product, 1.0)
     plan = _plan(product, system, 4)
     gpu = product.Simulation(system, settings, plan)
     orc = oracle_mod.OracleSimulation(system, settings, plan)
-    for chunk in (1, 2):
+    done = 0
+    for chunk in (1, 2, 100):
         gpu.run(chunk, threaded=False)
         orc.run(chunk)
-    assert_same(gpu, orc, "kochi-1.0")
+        done += chunk
+        if chunk != 2:
+            assert_same(gpu, orc, f"kochi-1.0 after {done} steps")
+    gpu.close()
 
 
 GPU_PHASES = {"momentum": ("momentum", "edges")}
