@@ -10,7 +10,8 @@ sm_100a CUDA kernels through the C ABI in ``include/tsunami_b200.h``.
 from .balance import (B200_MODEL, GPU_REFERENCE_MODEL, CostModel, DecompositionPlan, PlanError,
                       b200_block_weights, b200_phase_weights, concat_plans,
                       phase_balanced_plan, AssignmentPlan, packed_plan, equal_cell_plan, fit_cost_model, minmax_plan,
-                      predict_rank_cost, rank_costs)
+                      predict_rank_cost, rank_costs, save_cost_model, load_cost_model, measure_block_costs,
+                      measure_width_costs, save_width_costs, load_width_costs)
 from .grid import (Block, BoundaryConditions, GridLevel, GridStructureError, InitialCondition,
                    NestedGridSystem, SimulationConfig, build_kochi_scaled_config,
                    kochi_block_inventory, kochi_settings, level_abutments,
@@ -30,5 +31,6 @@ __all__ = [
     "build_kochi_scaled_config", "build_offset_tables", "concat_plans", "equal_cell_plan",
     "fit_cost_model", "kochi_block_inventory", "kochi_settings", "level_abutments",
     "minmax_plan", "predict_rank_cost", "rank_costs", "run_simulation",
-    "uncovered_side_intervals", "validate_system", "__version__",
+    "uncovered_side_intervals", "validate_system", "__version__", "save_cost_model", "load_cost_model",
+    "measure_block_costs", "measure_width_costs", "save_width_costs", "load_width_costs",
 ]

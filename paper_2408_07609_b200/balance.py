@@ -39,9 +39,137 @@ class CostModel:
 
 # The reference's canned GPU coefficients (balance.py:256).
 GPU_REFERENCE_MODEL = CostModel(slope=1.09e-4, intercept=46.2, r_squared=0.942)
-# B200 step cost of the flattened-tile kernels: blocks share launches, so the
-# per-block intercept is only the tile-quantisation tail.
-B200_MODEL = CostModel(slope=1.0 / 60.0e3, intercept=0.5)
+# The B200 step cost per block, fitted by measure_block_costs on a B200
+# (profiles/r02/costs/b200_cost_model.txt, tools/fit_costs.py: 60-wide
+# blocks of 6,000 .. 1.5 M cells sharing a step's launches, so the intercept
+# is only a tile-quantisation tail).
+B200_MODEL = CostModel(slope=4.3022e-05, intercept=0.2427, r_squared=0.99992)
+
+
+def save_cost_model(model: CostModel, path: str):
+    """The reference's model file (balance.py:77-81): ``key = repr`` lines."""
+    with open(path, "w") as f:
+        f.write(f"slope = {model.slope!r}\n")
+        f.write(f"intercept = {model.intercept!r}\n")
+        f.write(f"r_squared = {model.r_squared!r}\n")
+
+
+def load_cost_model(path: str) -> CostModel:
+    """Read a model file written by save_cost_model or by the reference's
+    (balance.py:84-94)."""
+    values = {}
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if not line or line.startswith("#"):
+                continue
+            key, _, val = line.partition("=")
+            values[key.strip()] = float(val)
+    return CostModel(slope=values["slope"], intercept=values["intercept"],
+                     r_squared=values.get("r_squared", float("nan")))
+
+
+def _copies_system(ni: int, nj: int, copies: int, depth: float, eta0):
+    """``copies`` identical, non-touching single-level blocks of ni x nj
+    cells (no exchanges between them) and settings with the given initial
+    level (a callable of the block index)."""
+    from .grid import Block, GridLevel, InitialCondition, NestedGridSystem, SimulationConfig
+    dx = 10.0
+    blocks = [Block(k + 1, (k * (ni + 8) * dx, 0.0), ni, nj, np.full((ni, nj), depth)) for k in range(copies)]
+    system = NestedGridSystem(levels=[GridLevel(1, dx, blocks)])
+    return system, SimulationConfig(dt=0.1, initial=eta0 or InitialCondition())
+
+
+class _RandomInitial:
+    """Small random initial displacement (as measure_momentum_cost,
+    balance.py:312-318), the same for every copy; duck-types
+    InitialCondition.eta0."""
+
+    kind = "random"
+
+    def __init__(self, ni, nj, seed):
+        self.ni, self.nj = ni, nj
+        self.field = 0.01 * np.random.default_rng(seed).standard_normal((ni, nj))
+
+    def eta0(self, x, y):
+        return self.field
+
+
+def measure_block_costs(cell_counts, repeats: int = 5, seed: int = 0, nj: int = 60, steps: int = 20,
+                        device: int | None = None, min_cells: float = 2e7):
+    """B200 replacement for the reference's host microbenchmark
+    measure_momentum_cost (balance.py:301-328): for each cell count, the
+    device time of one full step of a block of that size, as (cell_count,
+    microseconds) samples for :func:`fit_cost_model`.
+
+    A block timed alone leaves the GPU idle, so each sample times a step of
+    enough identical, non-touching copies (ni x ``nj`` cells each, 10 m deep
+    flat basin, the reference's small random displacement) to fill the
+    device, and divides by the copies: the marginal cost of the block inside
+    a step.  The median over ``repeats`` runs of ``steps`` steps (per-step
+    device events)."""
+    from .runner import Simulation
+    samples = []
+    for cells in cell_counts:
+        n_i = max(3, int(round(cells / nj)))
+        copies = max(1, int(np.ceil(min_cells / (n_i * nj))))
+        system, settings = _copies_system(n_i, nj, copies, 10.0, None)
+        settings.initial = _RandomInitial(n_i, nj, seed)
+        sim = Simulation(system, settings, device=0 if device is None else device)
+        try:
+            sim.run(3, threaded=False)
+            times = []
+            sim.set_timing(True)
+            for _ in range(repeats):
+                sim.run(steps, threaded=False)
+                times.append(sim.kernel_seconds()[2] * 1e6 / copies)
+        finally:
+            sim.close()
+        samples.append((n_i * nj, float(np.median(times))))
+    return samples
+
+
+def measure_width_costs(widths=(24, 36, 48, 60, 90), cells: float = 4e7, steps: int = 40,
+                        device: int | None = None):
+    """Per-cell B200 step cost by block width (the table packed_plan and
+    phase_balanced_plan weigh blocks with): for each width a single-level
+    system of identical non-touching blocks of that width (``cells`` in
+    total, many waves), mass and momentum device times from the per-step
+    events.  Returns {nj: {"mass_ps_per_cell", "momentum_ps_per_cell",
+    "step_ps_per_cell"}}."""
+    from .grid import InitialCondition
+    from .runner import Simulation
+    out = {}
+    for nj in widths:
+        ni = 2400
+        k = max(1, int(round(cells / (ni * nj))))
+        span = k * (ni + 8) * 10.0
+        system, settings = _copies_system(ni, nj, k, 200.0, InitialCondition(
+            "gaussian", 1.0, span / 6.0, (span / 2.0, nj * 5.0)))
+        sim = Simulation(system, settings, device=0 if device is None else device)
+        try:
+            sim.run(5, threaded=False)
+            sim.set_timing(True)
+            sim.run(steps, threaded=False)
+            m, mo, st = sim.kernel_seconds()
+        finally:
+            sim.close()
+        n = system.cell_count
+        out[int(nj)] = {"mass_ps_per_cell": m / n * 1e12, "momentum_ps_per_cell": mo / n * 1e12,
+                        "step_ps_per_cell": st / n * 1e12}
+    return out
+
+
+def save_width_costs(table: dict, path: str):
+    import json
+    with open(path, "w") as f:
+        json.dump({str(k): v for k, v in table.items()}, f, indent=1)
+
+
+def load_width_costs(path: str) -> dict:
+    import json
+    with open(path) as f:
+        return {int(k): v for k, v in json.load(f).items()}
 
 
 def fit_cost_model(samples) -> CostModel:
@@ -130,14 +258,15 @@ def equal_cell_plan(cells, n_ranks: int) -> DecompositionPlan:
     return DecompositionPlan(cells, tuple(seps))
 
 
-# Measured B200 cost per cell (ps) by block width: tools/fit_costs.py
-# (single-level systems of 40 M cells of one width, 40 steps; round-1
-# kernels).  The march gives a tile ceil((nj+3)/32) warps, or packs tiles of
-# nj + 3 threads into 128-thread CTAs (nj = 36), so widths just past a warp
-# multiple cost more per cell; the mass pass is per-cell memory work.
-B200_MASS_PS_BY_WIDTH = {24: 15.09, 36: 14.2, 48: 13.56, 60: 13.34, 90: 13.36}
-B200_MOMENTUM_PS_BY_WIDTH = {24: 36.42, 36: 32.65, 48: 37.49, 60: 29.18, 90: 29.29}
-B200_STEP_PS_BY_WIDTH = {24: 54.63, 36: 49.33, 48: 53.05, 60: 44.1, 90: 44.0}
+# Measured B200 cost per cell (ps) by block width: balance.measure_width_costs
+# (tools/fit_costs.py, profiles/r02/costs/b200_width_costs.json: single-level
+# systems of 40 M cells of one width, 40 steps).  The march gives a tile
+# ceil((nj+3)/32) warps, or packs tiles of nj + 3 threads into 128-thread
+# CTAs (nj = 36), so widths just past a warp multiple cost more per cell; the
+# mass pass is per-cell memory work.
+B200_MASS_PS_BY_WIDTH = {24: 14.43, 36: 13.90, 48: 13.45, 60: 13.33, 90: 13.61}
+B200_MOMENTUM_PS_BY_WIDTH = {24: 33.42, 36: 29.54, 48: 33.19, 60: 26.71, 90: 26.08}
+B200_STEP_PS_BY_WIDTH = {24: 50.86, 36: 45.82, 48: 48.60, 60: 41.58, 90: 41.03}
 
 
 def _lane_factor(nj: int) -> float:
@@ -164,16 +293,24 @@ def b200_step_ps_per_cell(nj: int, table=None) -> float:
     return base * (2.0 * _lane_factor(nj) / _lane_factor(ref) + 1.0) / 3.0
 
 
-def b200_phase_weights(system):
-    """(mass, momentum) B200 cost of every block (global order), ps/step."""
+def b200_phase_weights(system, table=None):
+    """(mass, momentum) B200 cost of every block (global order), ps/step;
+    ``table`` a measure_width_costs / load_width_costs result (default: the
+    committed B200 table above)."""
+    if table:
+        mass_t = {k: v["mass_ps_per_cell"] for k, v in table.items()}
+        mom_t = {k: v["momentum_ps_per_cell"] for k, v in table.items()}
+    else:
+        mass_t, mom_t = B200_MASS_PS_BY_WIDTH, B200_MOMENTUM_PS_BY_WIDTH
+    ref = 60 if 60 in mom_t else min(mom_t, key=lambda w: abs(w - 60))
     mass, mom = [], []
     for _, b in system.all_blocks():
         n = b.ni * b.nj
-        mass.append(n * B200_MASS_PS_BY_WIDTH.get(b.nj, 13.7))
-        if b.nj in B200_MOMENTUM_PS_BY_WIDTH:
-            mom.append(n * B200_MOMENTUM_PS_BY_WIDTH[b.nj])
+        mass.append(n * mass_t.get(b.nj, float(np.mean(list(mass_t.values())))))
+        if b.nj in mom_t:
+            mom.append(n * mom_t[b.nj])
         else:
-            mom.append(n * B200_MOMENTUM_PS_BY_WIDTH[60] * _lane_factor(b.nj) / _lane_factor(60))
+            mom.append(n * mom_t[ref] * _lane_factor(b.nj) / _lane_factor(ref))
     return mass, mom
 
 
@@ -186,13 +323,13 @@ def _phase_objective(seps, mass, mom):
     return max(pm) + max(pk) + 1e-3 * max(x + y for x, y in zip(pm, pk))
 
 
-def phase_balanced_plan(system, n_ranks: int) -> DecompositionPlan:
+def phase_balanced_plan(system, n_ranks: int, table=None) -> DecompositionPlan:
     """Consecutive-block plan minimising max(mass) + max(momentum) over
     ranks (the step's two big phases are separated by rank barriers, so
     balancing their sum is not enough): exhaustive for two ranks, else
     separator-wise descent from the min-max plan of the summed cost."""
     cells = tuple(b.ni * b.nj for _, b in system.all_blocks())
-    mass, mom = b200_phase_weights(system)
+    mass, mom = b200_phase_weights(system, table)
     n = len(cells)
     if n_ranks == 1:
         return DecompositionPlan(cells, ())
@@ -252,13 +389,13 @@ class AssignmentPlan:
         return [k for k, o in enumerate(self.owners) if o == rank]
 
 
-def packed_plan(system, n_ranks: int, sweeps: int = 50) -> AssignmentPlan:
+def packed_plan(system, n_ranks: int, sweeps: int = 50, table=None) -> AssignmentPlan:
     """Blocks packed onto ranks without the consecutive-run restriction:
     longest-processing-time placement by mass + momentum cost, then single
     moves and pairwise swaps that lower max(mass) + max(momentum) over ranks
     (the step's two barrier-separated phases).  Cross-rank exchanges cost
     little here (receive areas over NVLink), block granularity a lot."""
-    mass, mom = b200_phase_weights(system)
+    mass, mom = b200_phase_weights(system, table)
     n = len(mass)
     cells = tuple(b.ni * b.nj for _, b in system.all_blocks())
     if not 1 <= n_ranks <= n:

@@ -227,22 +227,29 @@ def cfl_limit(dx: float, dt: float, g: float = DEFAULT_GRAVITY) -> float:
 
 def check_system(system, settings) -> list[str]:
     """Structural pre-check of what the device path relies on: positive dt,
-    3:1 ratio, lattice alignment, block shapes and the CFL bound
-    (a subset of grid.validate_system, grid.py:242-318).  Returns messages."""
+    3:1 ratio, lattice alignment, block shapes and the CFL bound (a subset
+    of grid.validate_system, grid.py:242-318), in the reference's message
+    format (Violation.__str__, grid.py:163-177)."""
     out = []
     if not settings.dt > 0:
-        return [f"dt must be positive, got {settings.dt}"]
+        return [f"[timestep] level 0: dt must be positive, got {settings.dt}"]
     for k, lvl in enumerate(system.levels):
         if k and abs(system.levels[k - 1].dx / lvl.dx - REFINEMENT_RATIO) > 1e-9:
-            out.append(f"level {lvl.level_index}: dx {lvl.dx} is not parent dx / 3")
+            out.append(f"[ratio] level {lvl.level_index}: dx {lvl.dx} is not parent dx "
+                       f"{system.levels[k - 1].dx} / {REFINEMENT_RATIO}")
         for b in lvl.blocks:
             if b.ni < 1 or b.nj < 1:
-                out.append(f"block {b.block_id} is {b.ni}x{b.nj}")
+                out.append(f"[shape] level {lvl.level_index} block {b.block_id}: block is {b.ni}x{b.nj}, "
+                           "need at least 1x1")
             if np.shape(b.h) != (b.ni, b.nj):
-                out.append(f"block {b.block_id}: bathymetry shape {np.shape(b.h)}")
+                out.append(f"[bathymetry] level {lvl.level_index} block {b.block_id}: bathymetry shape "
+                           f"{np.shape(b.h)} != ({b.ni}, {b.nj})")
         hmax = max_water_depth(lvl)
-        if hmax > 0 and lvl.dx / settings.dt < math.sqrt(2.0 * settings.g * hmax):
-            out.append(f"level {lvl.level_index}: CFL violated (hmax {hmax:.6g})")
+        if hmax > 0:
+            wave = math.sqrt(2.0 * settings.g * hmax)
+            if lvl.dx / settings.dt < wave:
+                out.append(f"[cfl] level {lvl.level_index}: dx/dt = {lvl.dx / settings.dt:.6g} < "
+                           f"sqrt(2 g hmax) = {wave:.6g}")
     return out
 
 

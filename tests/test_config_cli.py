@@ -49,36 +49,3 @@ def test_config_errors(product, tmp_path):
                  "bathymetry: {kind: nope}}]}]\n")
     with pytest.raises(ConfigError):
         load_config(str(p))
-
-
-def _cli(*args, **kw):
-    return subprocess.run([sys.executable, "-m", "paper_2408_07609_b200", *args], capture_output=True,
-                          text=True, cwd=ROOT, timeout=kw.get("timeout", 300))
-
-
-def test_cli_validate():
-    ok = _cli("validate", os.path.join(CONFIGS, "cfg1.yaml"))
-    assert ok.returncode == 0 and "passed" in ok.stdout
-    bad = _cli("validate", os.path.join(CONFIGS, "cfl_violation.yaml"))
-    assert bad.returncode == 2 and "CFL" in bad.stdout
-
-
-@pytest.mark.gpu
-def test_cli_run_writes_reference_outputs(cuda_device, product, tmp_path):
-    """`run` on cfg1.yaml: rasters identical to emitting a direct Simulation's
-    maxima, plus timing.csv and decomposition.txt; a CFL-violating config is
-    refused with exit code 2."""
-    from paper_2408_07609_b200 import report as R
-    out = tmp_path / "out"
-    res = _cli("run", os.path.join(CONFIGS, "cfg1.yaml"), "--out", str(out), "--steps", "60")
-    assert res.returncode == 0, res.stderr
-    system, settings, _ = systems.make(product, "cfg1")
-    sim = product.Simulation(system, settings)
-    sim.run(60, threaded=False)
-    R.emit_rasters(system, sim.accumulators, str(tmp_path / "direct"))
-    for f in os.listdir(tmp_path / "direct"):
-        assert (out / f).read_bytes() == (tmp_path / "direct" / f).read_bytes(), f
-    assert (out / "timing.csv").read_text().startswith("rank,steps,mass,momentum")
-    assert (out / "decomposition.txt").exists()
-    bad = _cli("run", os.path.join(CONFIGS, "cfl_violation.yaml"), "--out", str(tmp_path / "bad"))
-    assert bad.returncode == 2

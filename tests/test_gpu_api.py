@@ -179,3 +179,30 @@ def test_end_to_end_host_buffers_match_fresh_run(cuda_device, product):
         assert np.array_equal(eo, fresh.states[bid].eta_old)
         for f in ("eta_new", "m_old", "m_new", "n_old", "n_new"):
             assert np.array_equal(getattr(sim.states[bid], f), getattr(fresh.states[bid], f)), f
+
+
+def test_cost_model_measured_fitted_saved_loaded_and_planned(cuda_device, product, tmp_path):
+    """(f)2: the B200 replacement of measure_momentum_cost (balance.py:301-328)
+    measures per-block step costs on the device, fit_cost_model fits them,
+    the reference's model file round-trips, and the plans use it; the
+    per-width table feeds packed_plan."""
+    P = product
+    samples = P.measure_block_costs([6000, 60000, 600000], repeats=2, steps=5, min_cells=2e6)
+    assert [c for c, _ in samples] == [6000, 60000, 600000] and all(t > 0 for _, t in samples)
+    assert samples[2][1] > samples[0][1]
+    model = P.fit_cost_model(samples)
+    assert model.slope > 0 and model.r_squared > 0.9
+    path = str(tmp_path / "model.txt")
+    P.save_cost_model(model, path)
+    back = P.load_cost_model(path)
+    assert back == model
+    system = P.build_kochi_scaled_config(0.01)
+    cells = [b.cell_count for _, b in system.all_blocks()]
+    plan = P.minmax_plan(cells, 4, back)
+    assert plan.n_ranks == 4 and P.rank_costs(plan, back).max() <= P.rank_costs(P.equal_cell_plan(cells, 4),
+                                                                                back).max() + 1e-9
+    table = P.measure_width_costs((36, 60), cells=4e6, steps=5)
+    assert set(table) == {36, 60} and all(v["step_ps_per_cell"] > 0 for v in table.values())
+    P.save_width_costs(table, str(tmp_path / "w.json"))
+    packed = P.packed_plan(system, 4, table=P.load_width_costs(str(tmp_path / "w.json")))
+    assert packed.n_ranks == 4 and sorted(set(packed.owners)) == [0, 1, 2, 3]
