@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 #define TS_OK 0
 #define TS_ERR_NUMERICS 1
@@ -57,9 +57,19 @@ typedef struct ts_block_desc {
     int32_t level;             /* 0-based level index */
     double dx;                 /* GridLevel.dx */
     double manning;            /* scalar Block.manning_n (used if nman_ext == NULL) */
-    const double *h_ext;       /* (ni+4)*(nj+4): BlockState.h_ext after fill_bathymetry_halos */
+    const double *h_ext;       /* (ni+4)*(nj+4): BlockState.h_ext after fill_bathymetry_halos,
+                                  or NULL with h_profile */
     const double *nman_ext;    /* NULL or (ni+4)*(nj+4): BlockState.n_ext (array case) */
     const double *eta0;        /* ni*nj interior initial level (runner.py:77-80) */
+    /* Device-side bathymetry setup: a block whose depth
+     * depends on one axis only (Block.h a broadcast view: the synthetic
+     * slope / coastal-profile kinds, config.py:41-70) passes that 1-D
+     * profile instead of h_ext; the device builds h_ext — edge replication
+     * (kernels.py:108-112) and the siblings' strips (exchange.py:281-300,
+     * applied at the first ts_run) — bit for bit. */
+    const double *h_profile;   /* NULL, or ni values (h_axis 0) / nj values (h_axis 1) */
+    int32_t h_axis;            /* 0: h[i, j] = h_profile[i]; 1: h[i, j] = h_profile[j] */
+    int32_t pad_;
 } ts_block_desc;
 
 /* exchange.HaloEntry (exchange.py:62-101); entries are passed in the

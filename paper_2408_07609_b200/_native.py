@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TSUNAMI_B200_LIB") or os.path.join(HERE, "libtsunami_b200.so")
 
 TS_OK, TS_ERR_NUMERICS, TS_ERR_CUDA, TS_ERR_INVALID = 0, 1, 2, 3
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 FIELDS = {"eta_old": 0, "eta_new": 1, "m_old": 2, "m_new": 3, "n_old": 4, "n_new": 5,
           "h_ext": 6, "max_eta": 7, "max_speed": 8, "max_inundation": 9}
@@ -31,7 +31,7 @@ PD = ctypes.POINTER(ctypes.c_double)
 class BlockDesc(ctypes.Structure):
     _fields_ = [("block_id", c_int64), ("ni", c_int32), ("nj", c_int32), ("owner", c_int32),
                 ("level", c_int32), ("dx", c_double), ("manning", c_double), ("h_ext", PD),
-                ("nman_ext", PD), ("eta0", PD)]
+                ("nman_ext", PD), ("eta0", PD), ("h_profile", PD), ("h_axis", c_int32), ("pad_", c_int32)]
 
 
 class HaloEntryC(ctypes.Structure):

@@ -123,6 +123,11 @@ struct ts_handle {
     bool p_two_pass = false;
     Copy *d_heta = nullptr, *d_hflux = nullptr, *d_edge = nullptr;
     int64_t n_heta = 0, n_hflux = 0, n_edge = 0;
+    // device-built bathymetry: the siblings' h strips, copied once before
+    // the first step (after every peer arena is mapped)
+    Copy *d_hfill = nullptr;
+    int64_t n_hfill = 0;
+    bool h_fill_pending = false;
     bool edge_serial = false;
     double *d_stage = nullptr;
     unsigned long long *d_err = nullptr;  // = d_sig + nranks + 1
@@ -524,8 +529,10 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (bd.ni < 1 || bd.nj < 1) return fail(TS_ERR_INVALID, "block %lld is %dx%d", (long long)bd.block_id, bd.ni, bd.nj);
         if (bd.owner < 0 || bd.owner >= h->nranks)
             return fail(TS_ERR_INVALID, "block %lld: owner %d outside [0, %d)", (long long)bd.block_id, bd.owner, h->nranks);
-        if (bd.owner == h->rank && (!bd.h_ext || !bd.eta0))
+        if (bd.owner == h->rank && ((!bd.h_ext && !bd.h_profile) || !bd.eta0))
             return fail(TS_ERR_INVALID, "block %lld: missing h_ext/eta0", (long long)bd.block_id);
+        if (bd.h_profile && bd.h_axis != 0 && bd.h_axis != 1)
+            return fail(TS_ERR_INVALID, "block %lld: h_axis %d", (long long)bd.block_id, bd.h_axis);
         const size_t P = pitch_of(bd.nj);
         const size_t cell = (size_t)(bd.ni + 4) * P + TS_BASE_SHIFT, mrows = (size_t)(bd.ni + 5) * P + TS_BASE_SHIFT;
         const size_t acc = (size_t)bd.ni * P;
@@ -579,9 +586,22 @@ int create_impl(const ts_desc *d, ts_handle *h)
         if (bd.owner != h->rank) continue;
         place_block(B, h->arena + h->off[b], B.has_nman != 0);
         const size_t P = B.P;
-        // h_ext / n_ext with ghosts (kernels.py:53-62, exchange.py:281-300)
-        CK(cudaMemcpy2D(B.h, P * 8, bd.h_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
-                        bd.ni + 4, cudaMemcpyHostToDevice));
+        // h_ext / n_ext with ghosts (kernels.py:53-62, exchange.py:281-300):
+        // copied, or built on the device from a 1-D profile
+        if (bd.h_ext) {
+            CK(cudaMemcpy2D(B.h, P * 8, bd.h_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
+                            bd.ni + 4, cudaMemcpyHostToDevice));
+        } else {
+            const int len = bd.h_axis == 0 ? bd.ni : bd.nj;
+            double *prof = nullptr;
+            CK(cudaMalloc((void **)&prof, (size_t)len * 8));
+            CK(cudaMemcpy(prof, bd.h_profile, (size_t)len * 8, cudaMemcpyHostToDevice));
+            launch_h_profile(B, prof, bd.h_axis, h->stream);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(h->stream));
+            CK(cudaFree(prof));
+            h->h_fill_pending = true;
+        }
         if (B.nman)
             CK(cudaMemcpy2D(B.nman, P * 8, bd.nman_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
                             bd.ni + 4, cudaMemcpyHostToDevice));
@@ -886,6 +906,19 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->n_heta = (int64_t)eta_own.size();
         h->n_hflux = (int64_t)flux_own.size();
         if (int rc = upload(&h->d_heta, eta_own)) return rc;
+        // the same strips of h: fill_bathymetry_halos (exchange.py:281-300)
+        // for device-built bathymetry (every rank whose blocks send)
+        {
+            bool any_profile = false;
+            for (int b = 0; b < h->nb; ++b) any_profile |= d->blocks[b].h_profile != nullptr;
+            if (any_profile) {
+                std::vector<Copy> hf = eta_own;
+                for (auto &c : hf) c.src_blk |= 3 << 28;
+                h->n_hfill = (int64_t)hf.size();
+                if (int rc = upload(&h->d_hfill, hf)) return rc;
+                h->h_fill_pending = h->n_hfill > 0;
+            }
+        }
         if (int rc = upload(&h->d_hflux, flux_own)) return rc;
     }
     // ---- outer-boundary edges (kernels.py:274-306)
@@ -936,6 +969,20 @@ int create_impl(const ts_desc *d, ts_handle *h)
     return get_graph(h, 0, &g);
 }
 
+// the siblings' bathymetry strips of device-built h_ext, once, before the
+// first step (peer arenas are mapped by then; the first step's halo-eta
+// barrier orders them before any rank's momentum reads ghost h)
+int fill_bathymetry(ts_handle *h)
+{
+    if (!h->h_fill_pending) return TS_OK;
+    if (h->imported != h->nranks - 1) return TS_OK;       // ts_run reports the missing peers
+    const StepArgs a = args_of(h, h->cur);
+    launch_copies(a, h->d_hfill, h->n_hfill, false, h->stream);
+    CK(cudaGetLastError());
+    h->h_fill_pending = false;
+    return TS_OK;
+}
+
 int check_error(ts_handle *h)
 {
     unsigned long long key;
@@ -984,6 +1031,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
         return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
                     h->rank, h->imported, h->nranks - 1);
     cudaStream_t s = h->stream;
+    if (int rc = fill_bathymetry(h)) return rc;
     // the first step of every run folds nothing: the previous run ended with
     // the flush (or no step ran yet), and host writes made since then must
     // not reach the maxima (the reference folds only in a step's output
@@ -1105,6 +1153,7 @@ int ts_phase(ts_handle *h, int32_t phase)
     if (!h) return fail(TS_ERR_INVALID, "null handle");
     CK(cudaSetDevice(h->device));
     cudaStream_t s = h->stream;
+    if (int rc = fill_bathymetry(h)) return rc;
     const StepArgs a = args_of(h, h->cur);
     switch (phase) {
     case TS_PH_MASS: launch_mass(a, h->d_all, h->n_all, false, s); break;
@@ -1143,6 +1192,8 @@ int ts_phase(ts_handle *h, int32_t phase)
 int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_t len)
 {
     if (!h || !out) return fail(TS_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    if (int rc = fill_bathymetry(h)) return rc;
     FieldGeom g;
     if (int rc = field_geom(h, block, field, &g)) return rc;
     if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
@@ -1158,6 +1209,8 @@ int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_
 int ts_set_field(ts_handle *h, int32_t block, int32_t field, const double *in, int64_t len)
 {
     if (!h || !in) return fail(TS_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    if (int rc = fill_bathymetry(h)) return rc;
     FieldGeom g;
     if (int rc = field_geom(h, block, field, &g)) return rc;
     if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
@@ -1263,6 +1316,7 @@ int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const doubl
 {
     if (!h || n < 0 || (n && (!blocks || !h_ext || !eta0))) return fail(TS_ERR_INVALID, "null argument");
     CK(cudaSetDevice(h->device));
+    if (int rc = fill_bathymetry(h)) return rc;
     size_t total = 0;
     for (int k = 0; k < n; ++k) {
         FieldGeom g;
@@ -1297,6 +1351,7 @@ int ts_download_fields(ts_handle *h, int32_t n, const int32_t *blocks, int32_t n
     if (!h || n < 0 || nf < 0 || (n && nf && (!blocks || !fields || !out)))
         return fail(TS_ERR_INVALID, "null argument");
     CK(cudaSetDevice(h->device));
+    if (int rc = fill_bathymetry(h)) return rc;
     std::vector<FieldGeom> geo((size_t)n * nf);
     size_t total = 0;
     for (int k = 0; k < n; ++k)
@@ -1395,6 +1450,7 @@ void ts_destroy(ts_handle *h)
     }
     cudaFree(h->d_recv);
     cudaFree(h->d_heta);
+    cudaFree(h->d_hfill);
     cudaFree(h->d_hflux);
     cudaFree(h->d_edge);
     cudaFree(h->d_stage);

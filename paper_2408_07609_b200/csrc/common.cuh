@@ -49,7 +49,8 @@ struct PSeg {
 };
 
 // element copy: dst[dst_idx] = src[src_idx]; arr 0 eta, 1 m, 2 n (the
-// "new" buffer of each); src_idx < 0 means "write 0" (reflective edge)
+// "new" buffer of each), 3 h (setup); src_idx < 0 means "write 0"
+// (reflective edge)
 struct Copy {
     int32_t src_blk, dst_blk, src_idx, dst_idx;   // src_blk holds arr in bits 28..29
 };
@@ -115,6 +116,8 @@ void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int
                     cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
+// h_ext of a block from a 1-D depth profile, ghosts edge-replicated
+void launch_h_profile(const DevBlock &B, const double *prof, int axis, cudaStream_t s);
 void launch_repitch(double *dst, int64_t dpitch, const double *src, int64_t spitch, int64_t rows, int64_t cols,
                     cudaStream_t s);
 // many pitched <-> contiguous copies in one launch (batched host transfers)

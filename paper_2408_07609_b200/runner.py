@@ -102,18 +102,37 @@ def _strip(ni, nj, side, span, sending, g=HALO_WIDTH):
     return slice(g + lo, g + hi), ys
 
 
-def host_block_arrays(system, settings, pinned: bool = False):
+def h_profile(block):
+    """(axis, 1-D profile) when the block's depth depends on one axis only —
+    Block.h a broadcast view (stride 0 along the other axis: the synthetic
+    coastal-profile and x- or y-only slope kinds) — else None."""
+    h = block.h
+    if not isinstance(h, np.ndarray) or h.ndim != 2 or h.dtype != np.float64 or h.shape != (block.ni, block.nj):
+        return None
+    if h.strides[1] == 0:
+        return 0, np.ascontiguousarray(h[:, 0])
+    if h.strides[0] == 0:
+        return 1, np.ascontiguousarray(h[0, :])
+    return None
+
+
+def host_block_arrays(system, settings, pinned: bool = False, device_bathymetry: bool = False):
     """Per block id: ghosted h_ext, optional n_ext, interior eta0 — the
     reference's BlockState setup (kernels.py:39-62, 97-101), initial
     sampling (runner.py:75-80) and fill_bathymetry_halos (exchange.py:281-300).
-    ``pinned``: h_ext and eta0 in page-locked memory (ts_host_alloc)."""
+    ``pinned``: h_ext and eta0 in page-locked memory (ts_host_alloc).
+    ``device_bathymetry``: h_ext is None for blocks with a 1-D depth profile
+    (h_profile): the device builds it (ts_block_desc.h_profile)."""
     g = HALO_WIDTH
     out = {}
     for lvl in system.levels:
         for b in lvl.blocks:
-            h = np.empty((b.ni + 2 * g, b.nj + 2 * g))
-            h[g:g + b.ni, g:g + b.nj] = np.asarray(b.h, dtype=float)
-            _replicate_halo(h)
+            if device_bathymetry and h_profile(b) is not None:
+                h = None
+            else:
+                h = np.empty((b.ni + 2 * g, b.nj + 2 * g))
+                h[g:g + b.ni, g:g + b.nj] = np.asarray(b.h, dtype=float)
+                _replicate_halo(h)
             if np.ndim(b.manning_n) == 0:
                 nman = None
             else:
@@ -131,6 +150,8 @@ def host_block_arrays(system, settings, pinned: bool = False):
             hp[...] = h
             ep[...] = eta0
             out[bid] = (hp, nman, ep)
+    if device_bathymetry:
+        return out
     for lvl in system.levels:
         starts = {b.block_id: lattice_origin(b, lvl.dx) for b in lvl.blocks}
         dims = {b.block_id: (b.ni, b.nj) for b in lvl.blocks}
@@ -157,7 +178,11 @@ def build_descriptor(system, settings, owner, halo, tables, domain_edges_by_rank
     restriction/prolongation segments and the domain-edge rules.  Accepts the
     reference's own objects (duck-typed).  Returns (desc, keepalive)."""
     ordered = system.all_blocks()
-    arrays = host_block_arrays(system, settings)
+    # bathymetry with a 1-D depth profile is built on the device; the
+    # siblings' strips are then copied on the device for every block (from
+    # whichever h the sender has), so the host skips them
+    profiled = any(h_profile(b) is not None for _, b in ordered)
+    arrays = host_block_arrays(system, settings, device_bathymetry=profiled)
     keep = []
     blocks = (N.BlockDesc * len(ordered))()
     for k, (lvl, b) in enumerate(ordered):
@@ -168,7 +193,14 @@ def build_descriptor(system, settings, owner, halo, tables, domain_edges_by_rank
         d.level = system.levels.index(lvl)
         d.dx = lvl.dx
         d.manning = float(b.manning_n) if nman is None else 0.0
-        d.h_ext = h.ctypes.data_as(N.PD)
+        if h is None:
+            axis, prof = h_profile(b)
+            keep.append(prof)
+            d.h_ext = None
+            d.h_profile = prof.ctypes.data_as(N.PD)
+            d.h_axis = axis
+        else:
+            d.h_ext = h.ctypes.data_as(N.PD)
         d.nman_ext = nman.ctypes.data_as(N.PD) if nman is not None else None
         d.eta0 = eta0.ctypes.data_as(N.PD)
     idx = {b.block_id: k for k, (_, b) in enumerate(ordered)}

@@ -146,10 +146,12 @@ def cfg5(T, scale=1.0, strips=8, rows=None):
     blocks = []
     for k in range(strips):
         o = (k * ni * dx, 0.0)
+        # x-only depths as broadcast views (the same values as full arrays;
+        # the product builds such bathymetry on the device, runner.h_profile)
         if k < strips - 1:
-            h = np.full((ni, nj), 50.0)
+            h = np.broadcast_to(np.full((ni, 1), 50.0), (ni, nj))
         else:
-            h = slope(o, ni, nj, dx, 50.0 + 0.01 * x_last, -0.01)
+            h = np.broadcast_to(slope(o, ni, 1, dx, 50.0 + 0.01 * x_last, -0.01), (ni, nj))
         blocks.append(T.Block(k + 1, o, ni, nj, h, 0.025))
     system = T.NestedGridSystem(levels=[T.GridLevel(1, dx, blocks)])
     sigma = 0.01 * max(wx, wy)

@@ -206,3 +206,18 @@ def test_cost_model_measured_fitted_saved_loaded_and_planned(cuda_device, produc
     P.save_width_costs(table, str(tmp_path / "w.json"))
     packed = P.packed_plan(system, 4, table=P.load_width_costs(str(tmp_path / "w.json")))
     assert packed.n_ranks == 4 and sorted(set(packed.owners)) == [0, 1, 2, 3]
+
+
+@pytest.mark.parametrize("name", ("kochi", "cfg5"))
+def test_device_built_bathymetry_equals_host_setup(cuda_device, product, name):
+    """(f)3: blocks whose depth is a 1-D profile get h_ext built on the
+    device (edge replication + the siblings' strips), bit-identical to the
+    host setup (kernels.py:108-112, exchange.py:281-300)."""
+    from paper_2408_07609_b200.runner import h_profile, host_block_arrays
+    system, settings, _ = systems.kochi(product, 0.001) if name == "kochi" else systems.cfg5(product, 0.02)
+    assert all(h_profile(b) is not None for _, b in system.all_blocks())
+    host = host_block_arrays(system, settings)
+    sim = product.Simulation(system, settings)
+    for bid, st in sim.states.items():
+        assert np.array_equal(st.h_ext.view(np.uint64), host[bid][0].view(np.uint64)), bid
+    sim.close()
