@@ -66,6 +66,11 @@ struct Group {
     int T = 64;                         // march rows per tile of this group
     std::vector<Tile> tiles;
     Tile *d = nullptr;
+    // multi-GPU overlap: tiles[0, n_early) read no cell that the exchange
+    // chain (peers' halo / restriction stores, the received restriction,
+    // the halo copies that must follow it) writes, so they march while it
+    // runs; tiles[n_early, size) march after it
+    int n_early = 0;
 };
 
 }  // namespace
@@ -92,6 +97,9 @@ struct ts_handle {
     bool mom_par = true;
     cudaStream_t side[7] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[7] = {};
+    // the late tiles' branches (multi-stream overlap of the eta exchange)
+    cudaStream_t side2[7] = {};
+    cudaEvent_t ev_fork2 = nullptr, ev_join2[7] = {};
     // contiguous device staging of host transfers (one 1-D copy + repitch
     // kernel instead of a row-by-row 2-D copy of narrow rows)
     double *d_io = nullptr;
@@ -123,6 +131,15 @@ struct ts_handle {
     bool p_two_pass = false;
     Copy *d_heta = nullptr, *d_hflux = nullptr, *d_edge = nullptr;
     int64_t n_heta = 0, n_hflux = 0, n_edge = 0;
+    // halo-eta copies whose source a peer's restriction writes: after the
+    // received restriction (the reference's restriction-before-halo order),
+    // with a second barrier when one of them crosses ranks
+    Copy *d_heta2 = nullptr;
+    int64_t n_heta2 = 0;
+    bool x_halo2 = false;
+    bool overlap = false;                 // the exchange chain runs beside the early march tiles
+    cudaStream_t xs = nullptr;            // its stream
+    cudaEvent_t ev_xfork = nullptr, ev_xjoin = nullptr;
     // device-built bathymetry: the siblings' h strips, copied once before
     // the first step (after every peer arena is mapped)
     Copy *d_hfill = nullptr;
@@ -208,43 +225,87 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
     // restriction: this rank's sources (direct / staged / into peers'
     // receive areas), the second pass of a two-pass exchange, then - once
     // every rank's stores have landed - the values received from peers
-    if (h->r_send.nch) { launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, s); ++n; }
-    if (h->r_local.nch) { launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, s); ++n; }
-    if (h->x_restrict) { barrier(h, s); ++n; }
-    if (h->r_recv.nch) { launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, s); ++n; }
-    if (mark(2)) return TS_ERR_CUDA;
-    if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, s); ++n; }
-    if (h->x_halo) { barrier(h, s); ++n; }
-    if (mark(3)) return TS_ERR_CUDA;
-    {
-        // largest group on the main stream, the others forked onto side
-        // streams (parallel branches of the captured graph) and joined back
+    // momentum launches of one tile range of every width group: the
+    // largest on stream s, the others forked onto side streams (parallel
+    // branches of the captured graph) and joined back
+    auto march = [&](int which, cudaStream_t s) -> int {   // 0 all, 1 early, 2 late tiles
         int order[8], ng = 0;
-        for (int k = 0; k < (int)h->groups.size() && ng < 8; ++k)
-            if (!h->groups[k].tiles.empty()) order[ng++] = k;
+        auto range = [&](const Group &g, int &lo, int &cnt) {
+            lo = which == 2 ? g.n_early : 0;
+            cnt = which == 0 ? (int)g.tiles.size() : (which == 1 ? g.n_early : (int)g.tiles.size() - g.n_early);
+        };
+        for (int k = 0; k < (int)h->groups.size() && ng < 8; ++k) {
+            int lo, cnt;
+            range(h->groups[k], lo, cnt);
+            if (cnt > 0) order[ng++] = k;
+        }
         auto work = [&](int k) {
             const Group &g = h->groups[k];
-            return (double)g.tiles.size() * (g.lanes ? g.lanes : 32 * g.W);
+            int lo, cnt;
+            range(g, lo, cnt);
+            return (double)cnt * (g.lanes ? g.lanes : 32 * g.W);
         };
         for (int x = 1; x < ng; ++x)
             for (int y = x; y > 0 && work(order[y]) > work(order[y - 1]); --y)
                 std::swap(order[y], order[y - 1]);
         const bool par = h->mom_par && ng > 1;
-        if (par) CK(cudaEventRecord(h->ev_fork, s));
+        cudaStream_t *side = which == 2 ? h->side2 : h->side;
+        cudaEvent_t fork = which == 2 ? h->ev_fork2 : h->ev_fork;
+        cudaEvent_t *join = which == 2 ? h->ev_join2 : h->ev_join;
+        if (par) CK(cudaEventRecord(fork, s));
         for (int x = 0; x < ng; ++x) {
             Group &gr = h->groups[order[x]];
+            int lo, cnt;
+            range(gr, lo, cnt);
             cudaStream_t st = s;
             if (par && x > 0) {
-                st = h->side[x - 1];
-                CK(cudaStreamWaitEvent(st, h->ev_fork, 0));
+                st = side[x - 1];
+                CK(cudaStreamWaitEvent(st, fork, 0));
             }
-            launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, gr.lanes, st);
+            launch_momentum(a, gr.d + lo, cnt, gr.W, gr.T, gr.lanes, st);
             ++n;
             if (par && x > 0) {
-                CK(cudaEventRecord(h->ev_join[x - 1], st));
-                CK(cudaStreamWaitEvent(s, h->ev_join[x - 1], 0));
+                CK(cudaEventRecord(join[x - 1], st));
+                CK(cudaStreamWaitEvent(s, join[x - 1], 0));
             }
         }
+        return TS_OK;
+    };
+    // the eta exchange chain: restriction (this rank's sources, the second
+    // pass of a two-pass exchange), halo-eta, then - once every rank's
+    // stores have landed - the values peers restricted into this rank's
+    // blocks and the halo copies that read them
+    auto chain = [&](cudaStream_t c) -> int {
+        if (h->r_send.nch) { launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, c); ++n; }
+        if (h->r_local.nch) { launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, c); ++n; }
+        if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, c); ++n; }
+        if (h->x_restrict || h->x_halo) { barrier(h, c); ++n; }
+        if (h->r_recv.nch) { launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, c); ++n; }
+        if (h->n_heta2) { launch_copies(a, h->d_heta2, h->n_heta2, false, c); ++n; }
+        if (h->x_halo2) { barrier(h, c); ++n; }
+        CK(cudaGetLastError());
+        return TS_OK;
+    };
+    if (h->overlap) {
+        // DESIGN.md §5/§7: the chain and then the march of the tiles that
+        // read a cell it writes ("late" tiles: parents' ring lines, ghost
+        // strips) on their own stream, beside the march of every other tile
+        // - the finest level is never a parent, so most of the step's march
+        // overlaps the whole exchange (peer stores and barriers included)
+        CK(cudaEventRecord(h->ev_xfork, s));
+        CK(cudaStreamWaitEvent(h->xs, h->ev_xfork, 0));
+        if (int rc = chain(h->xs)) return rc;
+        if (mark(2)) return TS_ERR_CUDA;
+        if (mark(3)) return TS_ERR_CUDA;
+        if (int rc = march(2, h->xs)) return rc;
+        CK(cudaEventRecord(h->ev_xjoin, h->xs));
+        if (int rc = march(1, s)) return rc;
+        CK(cudaStreamWaitEvent(s, h->ev_xjoin, 0));
+    } else {
+        if (int rc = chain(s)) return rc;
+        if (mark(2)) return TS_ERR_CUDA;
+        if (mark(3)) return TS_ERR_CUDA;
+        if (int rc = march(0, s)) return rc;
     }
     if (mark(4)) return TS_ERR_CUDA;
     if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
@@ -511,6 +572,18 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaSetDevice(h->device));
     CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     for (auto &st : h->side) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    // the exchange chain and the late tiles on high-priority streams: their
+    // CTAs are dispatched ahead of the early tiles' remaining ones
+    {
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CK(cudaStreamCreateWithPriority(&h->xs, cudaStreamNonBlocking, hi));
+        for (auto &st : h->side2) CK(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, hi));
+    }
+    CK(cudaEventCreateWithFlags(&h->ev_fork2, cudaEventDisableTiming));
+    for (auto &e : h->ev_join2) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_xfork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&h->ev_xjoin, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     for (auto &e : h->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : h->ev) CK(cudaEventCreate(&e));
@@ -710,9 +783,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
                 gr.tiles.push_back(Tile{b, i0, std::min(i0 + T, ni + 1), j0, j1, 0});
         }
     }
-    for (auto &gr : h->groups) {
-        if (int rc = upload(&gr.d, gr.tiles)) return rc;
-    }
+    // (the march tiles are uploaded once the exchange tables below have
+    // split them into early and late ones)
     {
         // cell tiles of the flat kernels (mass + fold, flush): about
         // mass_cells cells each, whole rows up to 1024 columns
@@ -900,12 +972,76 @@ int create_impl(const ts_desc *d, ts_handle *h)
         }
         eta = dedup_last(eta);
         flux = dedup_last(flux);
-        std::vector<Copy> eta_own, flux_own;
-        for (auto &c : eta) if (owned(c.src_blk & 0x0fffffff)) eta_own.push_back(c);
+        // cells a peer's restriction writes (parent ring lines of a child
+        // on another rank): a halo copy reading one must follow the
+        // received restriction
+        std::unordered_set<long long> xr;
+        auto ckey = [](int b, long long idx) { return ((long long)b << 40) ^ idx; };
+        for (int k = 0; k < d->n_restrict; ++k) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            if (d->blocks[sg.child].owner == d->blocks[sg.parent].owner) continue;
+            const bool ns = sg.side >= TS_SOUTH;
+            const int Pp = h->hb[sg.parent].P;
+            for (int q = 0; q < sg.parent_hi - sg.parent_lo; ++q)
+                xr.insert(ckey(sg.parent, pidx(Pp, ns ? sg.parent_lo + q : sg.parent_line,
+                                               ns ? sg.parent_line : sg.parent_lo + q)));
+        }
+        std::vector<Copy> eta_own, eta_own2, flux_own;
+        for (auto &c : eta) {
+            const int sb = c.src_blk & 0x0fffffff;
+            const bool hazard = xr.count(ckey(sb, c.src_idx)) != 0;
+            if (hazard && d->blocks[sb].owner != d->blocks[c.dst_blk].owner) h->x_halo2 = true;
+            if (owned(sb)) (hazard ? eta_own2 : eta_own).push_back(c);
+        }
         for (auto &c : flux) if (owned(c.src_blk & 0x0fffffff)) flux_own.push_back(c);
         h->n_heta = (int64_t)eta_own.size();
+        h->n_heta2 = (int64_t)eta_own2.size();
         h->n_hflux = (int64_t)flux_own.size();
         if (int rc = upload(&h->d_heta, eta_own)) return rc;
+        if (int rc = upload(&h->d_heta2, eta_own2)) return rc;
+        // march tiles that read a cell the exchange chain writes on this
+        // rank (peers' halo stores, received restriction values, the halo
+        // copies after them) march after it; the others beside it
+        {
+            std::vector<std::vector<int>> late_rows(h->nb);
+            auto mark_row = [&](int b, int x) { late_rows[b].push_back(x); };
+            // every cell the chain writes into this rank's blocks: halo
+            // destinations (own copies and peers' stores) and restricted
+            // parent cells (whichever rank restricts them)
+            for (auto &c : eta)
+                if (owned(c.dst_blk)) mark_row(c.dst_blk, c.dst_idx / h->hb[c.dst_blk].P - TS_G);
+            for (int k = 0; k < d->n_restrict; ++k) {
+                const ts_eta_segment &sg = d->restrict_segs[k];
+                if (!owned(sg.parent)) continue;
+                const bool ns = sg.side >= TS_SOUTH;
+                for (int q = 0; q < sg.parent_hi - sg.parent_lo; ++q) mark_row(sg.parent, ns ? sg.parent_lo + q : sg.parent_line);
+            }
+            for (auto &v : late_rows) {
+                std::sort(v.begin(), v.end());
+                v.erase(std::unique(v.begin(), v.end()), v.end());
+            }
+            // measured: Kochi-1.0 2.061 vs 2.062 ms at 1 GPU,
+            // 0.763-0.770 vs 0.714 ms at 4 GPUs - the late tiles (every
+            // parent level's) start only after the chain and finish after the
+            // early ones; so opt-in (TSUNAMI_B200_OVERLAP=1)
+            h->overlap = false;
+            if (const char *f = getenv("TSUNAMI_B200_OVERLAP"))
+                h->overlap = atoi(f) != 0 && (!eta.empty() || d->n_restrict > 0);
+            for (auto &gr : h->groups) {
+                std::vector<Tile> early, late;
+                for (const Tile &t : gr.tiles) {
+                    // a tile reads cell rows [i0 - 2, i1]
+                    const auto &v = late_rows[t.blk];
+                    auto it = std::lower_bound(v.begin(), v.end(), t.i0 - 2);
+                    const bool is_late = h->overlap && it != v.end() && *it <= t.i1;
+                    (is_late ? late : early).push_back(t);
+                }
+                gr.n_early = (int)early.size();
+                gr.tiles = early;
+                gr.tiles.insert(gr.tiles.end(), late.begin(), late.end());
+                if (int rc = upload(&gr.d, gr.tiles)) return rc;
+            }
+        }
         // the same strips of h: fill_bathymetry_halos (exchange.py:281-300)
         // for device-built bathymetry (every rank whose blocks send)
         {
@@ -913,6 +1049,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
             for (int b = 0; b < h->nb; ++b) any_profile |= d->blocks[b].h_profile != nullptr;
             if (any_profile) {
                 std::vector<Copy> hf = eta_own;
+                hf.insert(hf.end(), eta_own2.begin(), eta_own2.end());
                 for (auto &c : hf) c.src_blk |= 3 << 28;
                 h->n_hfill = (int64_t)hf.size();
                 if (int rc = upload(&h->d_hfill, hf)) return rc;
@@ -1163,7 +1300,11 @@ int ts_phase(ts_handle *h, int32_t phase)
         if (h->x_restrict) barrier(h, s);
         launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, s);
         break;
-    case TS_PH_HALO_ETA: launch_copies(a, h->d_heta, h->n_heta, false, s); break;
+    case TS_PH_HALO_ETA:
+        launch_copies(a, h->d_heta, h->n_heta, false, s);
+        launch_copies(a, h->d_heta2, h->n_heta2, false, s);
+        if (h->x_halo || h->x_halo2) barrier(h, s);
+        break;
     case TS_PH_MOMENTUM:
         for (Group &gr : h->groups) {
             if (!gr.tiles.empty())
@@ -1477,6 +1618,15 @@ void ts_destroy(ts_handle *h)
         if (e) cudaEventDestroy(e);
     for (auto &st : h->side)
         if (st) cudaStreamDestroy(st);
+    if (h->xs) cudaStreamDestroy(h->xs);
+    for (auto &st : h->side2)
+        if (st) cudaStreamDestroy(st);
+    for (auto &e : h->ev_join2)
+        if (e) cudaEventDestroy(e);
+    if (h->ev_fork2) cudaEventDestroy(h->ev_fork2);
+    if (h->ev_xfork) cudaEventDestroy(h->ev_xfork);
+    if (h->ev_xjoin) cudaEventDestroy(h->ev_xjoin);
+    cudaFree(h->d_heta2);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
