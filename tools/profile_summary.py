@@ -1,6 +1,6 @@
 """Write profiles/ summaries from a tools/gpu_profile.sh TAG run.
 
-    python tools/profile_summary.py TAG      (reads gpurun_out/TAG_*)
+    python tools/profile_summary.py TAG [ROUND]     (reads gpurun_out/TAG_*; ROUND e.g. r02)
 """
 import collections
 import csv
@@ -12,6 +12,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
+rnd = sys.argv[2] if len(sys.argv) > 2 else "r01"
+title = {"r01": "Round 1", "r02": "Round 2"}.get(rnd, rnd)
 G, PR = os.path.join(ROOT, "gpurun_out"), os.path.join(ROOT, "profiles")
 
 rows = [r for r in csv.reader(open(os.path.join(G, f"{tag}_launches.csv"))) if len(r) > 10]
@@ -23,14 +25,14 @@ for r in rows[1:]:
     tot[k] += float(r[vi].replace(",", ""))
     cnt[k] += 1
 S = sum(tot.values())
-shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(PR, "r01_launches.csv"))
-with open(os.path.join(PR, "r01_launches.md"), "w") as f:
-    f.write("# Round 1 launch list (Kochi-1.0, 47,211,444 cells, 1 B200)\n\n")
+shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(PR, f"{rnd}_launches.csv"))
+with open(os.path.join(PR, f"{rnd}_launches.md"), "w") as f:
+    f.write(f"# {title} launch list (Kochi-1.0, 47,211,444 cells, 1 B200)\n\n")
     f.write("`ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 3 "
             "--warmup 3 --no-cpu` (tools/gpu_profile.sh): 12 graph steps (3 warm-up, 3 more while the "
             "clock sampler starts, 3 timed, 3 end-to-end) plus the end-of-run accumulator flush of each "
             "run and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch and "
-            "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group). Cold-cache, serialised per-launch times; the raw list is `r01_launches.csv`.\n\n")
+            "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group). Cold-cache, serialised per-launch times; the raw list is `" + rnd + "_launches.csv`.\n\n")
     f.write("| kernel | launches | total µs | share | avg µs |\n|---|---|---|---|---|\n")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         f.write(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {v / S * 100:.1f} % | {v / cnt[k] / 1e3:.1f} |\n")
@@ -58,15 +60,15 @@ for r in rows[2:]:
     kern.append(e)
 mom = [e for e in kern if "march" in e["kernel"]]
 traffic = sum(e["dram__bytes_read.sum"] + e["dram__bytes_write.sum"] for e in mom) * 1e9
-json.dump({"source": "profiles/r01_ncu_full.json (ncu --set full, Kochi-1.0, one step: the k_march launches)",
+json.dump({"source": f"profiles/{rnd}_ncu_full.json (ncu --set full, Kochi-1.0, one step: the k_march launches)",
            "kernel": "k_march", "bytes_per_step": traffic}, open(os.path.join(PR, "momentum_traffic.json"), "w"),
           indent=1)
 json.dump({"command": "tools/gpu_profile.sh: ncu --set full --clock-control none --import-source on "
                       "-k regex:'k_march|k_mass' --launch-skip 10 --launch-count 5 python bench.py --steps 2 "
                       "--warmup 3 --no-cpu", "kernels": kern},
-          open(os.path.join(PR, "r01_ncu_full.json"), "w"), indent=1)
-shutil.copy(os.path.join(G, f"{tag}_bench.json"), os.path.join(PR, "r01_bench_n1.json"))
-shutil.copy(os.path.join(G, f"{tag}_ref.json"), os.path.join(PR, "r01_bench_ref.json"))
+          open(os.path.join(PR, f"{rnd}_ncu_full.json"), "w"), indent=1)
+shutil.copy(os.path.join(G, f"{tag}_bench.json"), os.path.join(PR, f"{rnd}_bench_n1.json"))
+shutil.copy(os.path.join(G, f"{tag}_ref.json"), os.path.join(PR, f"{rnd}_bench_ref.json"))
 for e in kern:
     print(e["kernel"], e["gpu__time_duration.sum"], e["dram__bytes_read.sum"] + e["dram__bytes_write.sum"],
           e.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"))
