@@ -170,10 +170,17 @@ int ts_set_initial_eta(ts_handle *h, int32_t block, const double *eta0, int64_t 
  * and the step count.  Bathymetry and Manning n are kept. */
 int ts_reset(ts_handle *h);
 /* Batched host->device copy of the setup inputs of n owned blocks: h_ext
- * ((ni+4)*(nj+4), as ts_set_field(TS_H_EXT)) and the interior initial
- * level (ni*nj, as ts_set_initial_eta) — one synchronisation for all */
+ * ((ni+4)*(nj+4), as ts_set_field(TS_H_EXT); NULL leaves a block's
+ * bathymetry as is) and the interior initial level (ni*nj, as
+ * ts_set_initial_eta) — one synchronisation for all */
 int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const double *const *h_ext,
                      const double *const *eta0);
+/* The device-side setup of ts_block_desc.h_profile for n owned blocks
+ * again (a fresh run's bathymetry input): each 1-D depth profile (ni values
+ * for axes[k] 0, nj for 1) expands to h_ext with edge replication; the
+ * siblings' strips are copied before the next step */
+int ts_upload_profiles(ts_handle *h, int32_t n, const int32_t *blocks, const double *const *profiles,
+                       const int32_t *axes);
 /* Batched device->host copy of nf fields of n owned blocks in the
  * reference layout (as ts_get_field): out[k * nf + f] receives field
  * fields[f] of block blocks[k] — one synchronisation for all */

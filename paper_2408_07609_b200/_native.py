@@ -116,6 +116,7 @@ def lib():
     L.ts_reset.argtypes = [c_void_p]
     L.ts_upload_inputs.argtypes = [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]
     L.ts_download_fields.argtypes = [c_void_p, c_int32, c_void_p, c_int32, c_void_p, c_void_p]
+    L.ts_upload_profiles.argtypes = [c_void_p, c_int32, c_void_p, c_void_p, c_void_p]
     if L.ts_abi_version() != ABI_VERSION:
         raise ImportError(f"{LIB_PATH}: ABI {L.ts_abi_version()} != {ABI_VERSION}")
     _LIB = L
@@ -126,7 +127,7 @@ EXPORTED = ("ts_last_error", "ts_abi_version", "ts_create", "ts_run", "ts_phase"
             "ts_set_field", "ts_error_info", "ts_timings", "ts_steps_done", "ts_device_bytes",
             "ts_launches_per_step", "ts_set_timing", "ts_kernel_seconds", "ts_stream", "ts_destroy",
             "ts_ipc_export", "ts_ipc_import", "ts_cbrt_host", "ts_cbrt_device", "ts_set_initial_eta",
-            "ts_host_alloc", "ts_host_free", "ts_reset", "ts_upload_inputs", "ts_download_fields")
+            "ts_host_alloc", "ts_host_free", "ts_reset", "ts_upload_inputs", "ts_download_fields", "ts_upload_profiles")
 
 
 def pinned_empty(shape) -> np.ndarray:

@@ -71,6 +71,7 @@ struct Group {
     // the halo copies that must follow it) writes, so they march while it
     // runs; tiles[n_early, size) march after it
     int n_early = 0;
+    bool nman = false;                  // some block of the group has per-cell Manning n
 };
 
 }  // namespace
@@ -262,7 +263,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
                 st = side[x - 1];
                 CK(cudaStreamWaitEvent(st, fork, 0));
             }
-            launch_momentum(a, gr.d + lo, cnt, gr.W, gr.T, gr.lanes, st);
+            launch_momentum(a, gr.d + lo, cnt, gr.W, gr.T, gr.lanes, gr.nman, st);
             ++n;
             if (par && x > 0) {
                 CK(cudaEventRecord(join[x - 1], st));
@@ -776,6 +777,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
         int W, w;
         width_group(nj, W, w);
         Group &gr = h->groups[gid[b]];
+        gr.nman |= d->blocks[b].nman_ext != nullptr;
         const int T = gr.T;
         for (int j0 = 0; j0 < nj + 1; j0 += w) {
             const int j1 = std::min(j0 + w, nj + 1);
@@ -1047,14 +1049,12 @@ int create_impl(const ts_desc *d, ts_handle *h)
         {
             bool any_profile = false;
             for (int b = 0; b < h->nb; ++b) any_profile |= d->blocks[b].h_profile != nullptr;
-            if (any_profile) {
-                std::vector<Copy> hf = eta_own;
-                hf.insert(hf.end(), eta_own2.begin(), eta_own2.end());
-                for (auto &c : hf) c.src_blk |= 3 << 28;
-                h->n_hfill = (int64_t)hf.size();
-                if (int rc = upload(&h->d_hfill, hf)) return rc;
-                h->h_fill_pending = h->n_hfill > 0;
-            }
+            std::vector<Copy> hf = eta_own;
+            hf.insert(hf.end(), eta_own2.begin(), eta_own2.end());
+            for (auto &c : hf) c.src_blk |= 3 << 28;
+            h->n_hfill = (int64_t)hf.size();
+            if (int rc = upload(&h->d_hfill, hf)) return rc;
+            h->h_fill_pending = any_profile && h->n_hfill > 0;
         }
         if (int rc = upload(&h->d_hflux, flux_own)) return rc;
     }
@@ -1308,7 +1308,7 @@ int ts_phase(ts_handle *h, int32_t phase)
     case TS_PH_MOMENTUM:
         for (Group &gr : h->groups) {
             if (!gr.tiles.empty())
-                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, gr.lanes, s);
+                launch_momentum(a, gr.d, (int)gr.tiles.size(), gr.W, gr.T, gr.lanes, gr.nman, s);
         }
         break;
     case TS_PH_EDGES: launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); break;
@@ -1462,26 +1462,63 @@ int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const doubl
     for (int k = 0; k < n; ++k) {
         FieldGeom g;
         if (int rc = field_geom(h, blocks[k], TS_H_EXT, &g)) return rc;
-        if (!h_ext[k] || !eta0[k]) return fail(TS_ERR_INVALID, "block %d: null input", blocks[k]);
+        if (!eta0[k]) return fail(TS_ERR_INVALID, "block %d: null input", blocks[k]);
         const DevBlock &B = h->hb[blocks[k]];
-        total += (size_t)g.rows * g.cols + (size_t)B.ni * B.nj;
+        total += (h_ext[k] ? (size_t)g.rows * g.cols : 0) + (size_t)B.ni * B.nj;
     }
     if (int rc = bulk_reserve(h, total, 3 * (size_t)n)) return rc;
     std::vector<Repitch> jobs;
     size_t off = 0;
     for (int k = 0; k < n; ++k) {
         const DevBlock &B = h->hb[blocks[k]];
-        const size_t he = (size_t)(B.ni + 4) * (B.nj + 4), ee = (size_t)B.ni * B.nj;
+        const size_t he = h_ext[k] ? (size_t)(B.ni + 4) * (B.nj + 4) : 0, ee = (size_t)B.ni * B.nj;
         double *sh = h->d_bulk + off, *se = sh + he;
-        CK(cudaMemcpyAsync(sh, h_ext[k], he * 8, cudaMemcpyHostToDevice, h->stream));
+        if (he) {                          // (NULL: bathymetry left as is, e.g. ts_upload_profiles)
+            CK(cudaMemcpyAsync(sh, h_ext[k], he * 8, cudaMemcpyHostToDevice, h->stream));
+            jobs.push_back(Repitch{B.h, sh, B.P, B.nj + 4, B.ni + 4, B.nj + 4});
+        }
         CK(cudaMemcpyAsync(se, eta0[k], ee * 8, cudaMemcpyHostToDevice, h->stream));
-        jobs.push_back(Repitch{B.h, sh, B.P, B.nj + 4, B.ni + 4, B.nj + 4});
         // set_initial_eta: the interior of both water-level buffers
         for (int q = 0; q < 2; ++q)
             jobs.push_back(Repitch{B.eta[q] + 2 * (size_t)B.P + 2, se, B.P, B.nj, B.ni, B.nj});
         off += he + ee;
     }
     if (int rc = run_jobs(h, jobs)) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    return TS_OK;
+}
+
+int ts_upload_profiles(ts_handle *h, int32_t n, const int32_t *blocks, const double *const *profiles,
+                       const int32_t *axes)
+{
+    if (!h || n < 0 || (n && (!blocks || !profiles || !axes))) return fail(TS_ERR_INVALID, "null argument");
+    CK(cudaSetDevice(h->device));
+    if (int rc = fill_bathymetry(h)) return rc;
+    size_t total = 0;
+    for (int k = 0; k < n; ++k) {
+        FieldGeom g;
+        if (int rc = field_geom(h, blocks[k], TS_H_EXT, &g)) return rc;
+        if (!profiles[k] || (axes[k] != 0 && axes[k] != 1))
+            return fail(TS_ERR_INVALID, "block %d: bad profile", blocks[k]);
+        const DevBlock &B = h->hb[blocks[k]];
+        total += axes[k] == 0 ? B.ni : B.nj;
+    }
+    if (int rc = bulk_reserve(h, total, 0)) return rc;
+    size_t off = 0;
+    for (int k = 0; k < n; ++k) {
+        const DevBlock &B = h->hb[blocks[k]];
+        const size_t len = axes[k] == 0 ? B.ni : B.nj;
+        CK(cudaMemcpyAsync(h->d_bulk + off, profiles[k], len * 8, cudaMemcpyHostToDevice, h->stream));
+        launch_h_profile(B, h->d_bulk + off, axes[k], h->stream);
+        off += len;
+    }
+    CK(cudaGetLastError());
+    // the siblings' strips (exchange.py:281-300), once every rank's
+    // profiles are expanded: before this rank's next step
+    h->h_fill_pending = h->n_hfill > 0;
+    if (h->nranks == 1) {
+        if (int rc = fill_bathymetry(h)) return rc;
+    }
     CK(cudaStreamSynchronize(h->stream));
     return TS_OK;
 }

@@ -108,7 +108,9 @@ void launch_mass(const StepArgs &a, const Tile *tiles, int ntiles, bool accumula
 void launch_accumulate(const StepArgs &a, const Tile *tiles, int ntiles, cudaStream_t s);
 // lanes == 0: one tile per W warps (TPC tiles per CTA); lanes > 0: 128-thread
 // CTAs (W = 4) holding 128 / lanes tiles of `lanes` threads each
-void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, int lanes, cudaStream_t s);
+// nman: some tile's block has per-cell Manning n
+void launch_momentum(const StepArgs &a, const Tile *tiles, int ntiles, int W, int T, int lanes, bool nman,
+                     cudaStream_t s);
 int momentum_tiles_per_cta(int W, int lanes);
 void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, int nchunks, double *stage,
                      cudaStream_t s);

@@ -122,9 +122,12 @@ def host_block_arrays(system, settings, pinned: bool = False, device_bathymetry:
     sampling (runner.py:75-80) and fill_bathymetry_halos (exchange.py:281-300).
     ``pinned``: h_ext and eta0 in page-locked memory (ts_host_alloc).
     ``device_bathymetry``: h_ext is None for blocks with a 1-D depth profile
-    (h_profile): the device builds it (ts_block_desc.h_profile)."""
+    (h_profile): the device builds it (ts_block_desc.h_profile,
+    ts_upload_profiles) and copies every sibling strip; the host then skips
+    the strips of the other blocks too."""
     g = HALO_WIDTH
     out = {}
+    device_bathymetry = device_bathymetry and any(h_profile(b) is not None for _, b in system.all_blocks())
     for lvl in system.levels:
         for b in lvl.blocks:
             if device_bathymetry and h_profile(b) is not None:
@@ -146,9 +149,12 @@ def host_block_arrays(system, settings, pinned: bool = False, device_bathymetry:
             out[b.block_id] = (h, nman, eta0)
     if pinned:
         for bid, (h, nman, eta0) in out.items():
-            hp, ep = N.pinned_empty(h.shape), N.pinned_empty(eta0.shape)
-            hp[...] = h
+            ep = N.pinned_empty(eta0.shape)
             ep[...] = eta0
+            hp = None
+            if h is not None:
+                hp = N.pinned_empty(h.shape)
+                hp[...] = h
             out[bid] = (hp, nman, ep)
     if device_bathymetry:
         return out
@@ -579,13 +585,31 @@ class Simulation:
         items = sorted(self.states.items(), key=lambda kv: kv[1]._index)
         n = len(items)
         idx = (ctypes.c_int32 * max(1, n))(*[st._index for _, st in items])
-        hs = [np.ascontiguousarray(arrays[bid][0], dtype=float) for bid, _ in items]
+        # blocks whose h_ext is None (host_block_arrays(device_bathymetry=True))
+        # send their 1-D depth profile; the device expands it (§8(f)3)
+        blocks = {b.block_id: b for _, b in self.system.all_blocks()}
+        prof = [(st._index, h_profile(blocks[bid])) for bid, st in items if arrays[bid][0] is None]
+        hs = [None if arrays[bid][0] is None else np.ascontiguousarray(arrays[bid][0], dtype=float)
+              for bid, _ in items]
         es = [np.ascontiguousarray(arrays[bid][2], dtype=float) for bid, _ in items]
-        hp = (ctypes.c_void_p * max(1, n))(*[a.ctypes.data for a in hs])
+        nbytes = sum(a.nbytes for a in hs if a is not None) + sum(a.nbytes for a in es)
+        if prof:
+            if any(p is None for _, p in prof):
+                raise ValueError("h_ext missing for a block without a 1-D depth profile")
+            pi = (ctypes.c_int32 * len(prof))(*[k for k, _ in prof])
+            pv = [p[1] for _, p in prof]
+            pp = (ctypes.c_void_p * len(prof))(*[a.ctypes.data for a in pv])
+            pa = (ctypes.c_int32 * len(prof))(*[p[0] for _, p in prof])
+            N.check(N.lib().ts_upload_profiles(self._h, len(prof), pi, pp, pa))
+            nbytes += sum(a.nbytes for a in pv)
+            if self.world > 1:              # every rank's profiles expanded before any strip is copied
+                import torch.distributed as dist
+                dist.barrier(self.group)
+        hp = (ctypes.c_void_p * max(1, n))(*[0 if a is None else a.ctypes.data for a in hs])
         ep = (ctypes.c_void_p * max(1, n))(*[a.ctypes.data for a in es])
         N.check(N.lib().ts_upload_inputs(self._h, n, idx, hp, ep))
         self._invalidate()
-        return sum(a.nbytes for a in hs) + sum(a.nbytes for a in es)
+        return nbytes
 
     # the run's results (the rasters the reference's run writes, cli.py:160-176)
     RESULT_FIELDS = ("max_eta", "max_speed", "max_inundation")

@@ -221,3 +221,31 @@ def test_device_built_bathymetry_equals_host_setup(cuda_device, product, name):
     for bid, st in sim.states.items():
         assert np.array_equal(st.h_ext.view(np.uint64), host[bid][0].view(np.uint64)), bid
     sim.close()
+
+
+def test_end_to_end_with_device_bathymetry(cuda_device, product):
+    """The e2e leg on a system with 1-D depth profiles (Kochi): the profiles
+    are uploaded and expanded on the device instead of ghosted h_ext;
+    the result equals a fresh run."""
+    from paper_2408_07609_b200.runner import host_block_arrays
+    system, settings, _ = systems.kochi(product, 0.001)
+    fresh = product.Simulation(system, settings)
+    fresh.run(12, threaded=False)
+    sim = product.Simulation(system, settings)
+    sim.run(5, threaded=False)
+    sim.reset()
+    arrays = host_block_arrays(system, settings, pinned=True, device_bathymetry=True)
+    assert all(a[0] is None for a in arrays.values())
+    nbytes = sim.upload_initial_state(arrays)
+    assert nbytes < sum(a[2].nbytes for a in arrays.values()) * 1.1
+    sim.run(12, threaded=False)
+    outs = sim.output_buffers(pinned=True, fields=sim.RESULT_FIELDS)
+    got, _ = sim.download_outputs(outs)
+    for bid, maps in got.items():
+        for f, m in zip(sim.RESULT_FIELDS, maps):
+            assert np.array_equal(m.view(np.uint64), getattr(fresh.accumulators[bid], f).view(np.uint64)), (bid, f)
+        for f in ("eta_old", "m_old", "n_old", "h_ext"):
+            a, b = getattr(sim.states[bid], f), getattr(fresh.states[bid], f)
+            assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (bid, f)
+    sim.close()
+    fresh.close()
