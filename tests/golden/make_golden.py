@@ -198,6 +198,15 @@ def main():
         run_ref(sysn, T.SimulationConfig(dt=0.2), 3, 1)
     except K.NumericsError as exc:
         errs["nan_bathymetry"] = str(exc)
+    # wet_threshold 0 over a dry (h = 0, eta = 0) basin: every cell counts as
+    # wet, so the reference takes its all-wet branch (kernels.py, `if all_wet:`)
+    # and divides 0/0 -- a NumericsError, not a KernelFaultError.
+    sysd = T.NestedGridSystem(levels=[T.GridLevel(1, 10.0, [
+        T.Block(1, (0.0, 0.0), 6, 5, np.zeros((6, 5)))])])
+    try:
+        run_ref(sysd, T.SimulationConfig(dt=0.1, wet_threshold=0.0), 3, 1)
+    except K.NumericsError as exc:
+        errs["dry_basin_threshold0"] = str(exc)
     with open(os.path.join(HERE, "errors.json"), "w") as f:
         json.dump(errs, f, indent=1)
 

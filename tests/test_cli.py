@@ -185,6 +185,17 @@ def test_snapshots_and_trace(cuda_device, good_config, tmp_path):
                  "--out", str(out), "--no-figures"]) == 0
     names = os.listdir(out)
     assert any("step3" in n for n in names) and any("step6" in n for n in names)
+    # the snapshot written beside the next chunk holds that step's maxima
+    import paper_2408_07609_b200 as P
+    from paper_2408_07609_b200 import report as R
+    from paper_2408_07609_b200.config import load_config
+    system, settings = load_config(good_config)
+    sim = P.Simulation(system, settings, P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], 2))
+    sim.run(3, threaded=False)
+    R.emit_rasters(system, sim.accumulators, str(tmp_path / "direct"), tag="_step3")
+    for f in os.listdir(tmp_path / "direct"):
+        assert (out / f).read_bytes() == (tmp_path / "direct" / f).read_bytes(), f
+    sim.close()
     trace = tmp_path / "msg.bin"
     assert main(["run", "--config", good_config, "--steps", "2", "--workers", "2", "--trace", str(trace),
                  "--out", str(tmp_path / "tr"), "--no-figures"]) == 0

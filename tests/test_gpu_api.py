@@ -33,6 +33,20 @@ def test_numerics_error_message_matches_reference(cuda_device, product):
     assert str(ei.value) == want
 
 
+def test_numerics_error_dry_basin_threshold0(cuda_device, product):
+    """wet_threshold 0 over a dry basin: the reference's all-wet branch
+    divides 0/0 and raises NumericsError (golden made by the reference)."""
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        want = json.load(f)["dry_basin_threshold0"]
+    T = product
+    system = T.NestedGridSystem(levels=[T.GridLevel(1, 10.0, [
+        T.Block(1, (0.0, 0.0), 6, 5, np.zeros((6, 5)))])])
+    sim = T.Simulation(system, T.SimulationConfig(dt=0.1, wet_threshold=0.0), _plan(T, system, 1))
+    with pytest.raises(T.NumericsError) as ei:
+        sim.run(3, threaded=False)
+    assert str(ei.value) == want
+
+
 def test_worker_failure_aborts_threaded_run(cuda_device, product):
     """tests/test_runner.py:102-112: multi-rank runs wrap it in SimulationAborted."""
     system = _nan_system(product)

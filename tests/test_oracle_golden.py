@@ -158,6 +158,18 @@ def test_oracle_error_message(oracle_mod, product):
     assert str(ei.value) == want
 
 
+def test_oracle_error_message_dry_basin_threshold0(oracle_mod, product):
+    with open(os.path.join(GOLDEN, "errors.json")) as f:
+        want = json.load(f)["dry_basin_threshold0"]
+    T = product
+    system = T.NestedGridSystem(levels=[T.GridLevel(1, 10.0, [
+        T.Block(1, (0.0, 0.0), 6, 5, np.zeros((6, 5)))])])
+    sim = oracle_mod.OracleSimulation(system, T.SimulationConfig(dt=0.1, wet_threshold=0.0))
+    with pytest.raises(oracle_mod.OracleNumericsError) as ei:
+        sim.run(3)
+    assert str(ei.value) == want
+
+
 def test_oracle_kochi6h_first_checkpoint(oracle_mod, product):
     """The 6-hour golden's first checkpoint (1000 steps of Kochi-0.001 on the
     cbrt-aligned reference); the full 37,000-step run and the reference's
