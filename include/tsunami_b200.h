@@ -197,6 +197,18 @@ int64_t ts_steps_done(ts_handle *h);
 int64_t ts_device_bytes(ts_handle *h);
 /* kernels launched per ts_run step (graph nodes) */
 int32_t ts_launches_per_step(ts_handle *h);
+/* diagnostic: run ONE step (collective across ranks, like ts_run(1) without
+ * the end-of-run fold) as a graph with an event after every launch, the
+ * width groups' march launches serialised; for launch k, labels[k] = kind * 16
+ * + group and us[k] = device microseconds since the previous launch ended.
+ * Kinds: 0 mass, 1 restrict (sources), 2 restrict (second pass), 3 halo-eta,
+ * 4 barrier (label 64 eta, 65 second eta, 66 prolongation), 5 restrict
+ * (received), 6 halo-eta after the received restriction, 7 march (group),
+ * 8 edges, 9 prolong (sources), 10 prolong (second pass), 11 prolong
+ * (received), 12 halo-flux, 13 merged eta phase, 14 merged flux phase (the
+ * received values of a merged phase: labels 80 / 176).  *count = launches in the step (up to cap
+ * reported). */
+int ts_trace_step(ts_handle *h, int32_t *labels, float *us, int32_t cap, int32_t *count);
 /* timing mode: every 8th graph-replayed step of ts_run records the mass,
  * momentum and whole-step boundaries into its own CUDA events (on the launch
  * stream; rebinding a launch's event nodes costs it ~9 us, so the steps in

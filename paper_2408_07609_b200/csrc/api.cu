@@ -170,6 +170,16 @@ struct ts_handle {
     bool timing = false;
     cudaGraphNode_t ev_node[2][kPhaseEvents] = {};
     std::vector<cudaEvent_t> pool;                    // 5 per timed step
+    // merged exchange phases (build_merged): [0] eta sources, [1] eta
+    // received, [2] flux sources, [3] flux received
+    bool merged = false;
+    bool mx_bar_eta = false, mx_bar_flux = false;
+    XOp *d_mx[4] = {};
+    int64_t n_mx[4] = {};
+    // ts_trace_step: an event after every launch of one captured step
+    bool tracing = false;
+    std::vector<cudaEvent_t> trace_ev;
+    std::vector<int32_t> trace_label;
 };
 
 namespace {
@@ -217,8 +227,19 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
             CK(cudaEventRecord(h->ev[k], s));
         return 0;
     };
+    // ts_trace_step: an external event after every launch, labelled with
+    // the launch's kind (TS_TRACE_* of the header) * 16 + its group
+    auto tick = [&](cudaStream_t st, int label) -> int {
+        if (!h->tracing) return 0;
+        const size_t k = h->trace_label.size();
+        if (k >= h->trace_ev.size()) return 0;
+        CK(cudaEventRecordWithFlags(h->trace_ev[k], st, cudaEventRecordExternal));
+        h->trace_label.push_back(label);
+        return 0;
+    };
+    if (tick(s, -1)) return TS_ERR_CUDA;
     if (mark(0)) return TS_ERR_CUDA;
-    if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; }
+    if (h->n_all) { launch_mass(a, h->d_all, h->n_all, true, s); ++n; if (tick(s, 0)) return TS_ERR_CUDA; }
     if (mark(1)) return TS_ERR_CUDA;
     // multi-GPU phase barriers: only around phases with
     // cross-rank stores; each one orders this rank's peer stores before the
@@ -249,7 +270,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
         for (int x = 1; x < ng; ++x)
             for (int y = x; y > 0 && work(order[y]) > work(order[y - 1]); --y)
                 std::swap(order[y], order[y - 1]);
-        const bool par = h->mom_par && ng > 1;
+        const bool par = h->mom_par && ng > 1 && !h->tracing;
         cudaStream_t *side = which == 2 ? h->side2 : h->side;
         cudaEvent_t fork = which == 2 ? h->ev_fork2 : h->ev_fork;
         cudaEvent_t *join = which == 2 ? h->ev_join2 : h->ev_join;
@@ -265,6 +286,7 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
             }
             launch_momentum(a, gr.d + lo, cnt, gr.W, gr.T, gr.lanes, gr.nman, st);
             ++n;
+            if (tick(st, 7 * 16 + order[x])) return TS_ERR_CUDA;
             if (par && x > 0) {
                 CK(cudaEventRecord(join[x - 1], st));
                 CK(cudaStreamWaitEvent(s, join[x - 1], 0));
@@ -277,16 +299,36 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
     // stores have landed - the values peers restricted into this rank's
     // blocks and the halo copies that read them
     auto chain = [&](cudaStream_t c) -> int {
-        if (h->r_send.nch) { launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, c); ++n; }
-        if (h->r_local.nch) { launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, c); ++n; }
-        if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, c); ++n; }
-        if (h->x_restrict || h->x_halo) { barrier(h, c); ++n; }
-        if (h->r_recv.nch) { launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, c); ++n; }
-        if (h->n_heta2) { launch_copies(a, h->d_heta2, h->n_heta2, false, c); ++n; }
-        if (h->x_halo2) { barrier(h, c); ++n; }
+        if (h->r_send.nch) { launch_restrict(a, h->r_send.d, h->r_send.ch, h->r_send.nch, h->d_stage, c); ++n; if (tick(c, 16)) return TS_ERR_CUDA; }
+        if (h->r_local.nch) { launch_restrict(a, h->r_local.d, h->r_local.ch, h->r_local.nch, h->d_stage, c); ++n; if (tick(c, 32)) return TS_ERR_CUDA; }
+        if (h->n_heta) { launch_copies(a, h->d_heta, h->n_heta, false, c); ++n; if (tick(c, 48)) return TS_ERR_CUDA; }
+        if (h->x_restrict || h->x_halo) { barrier(h, c); ++n; if (tick(c, 64)) return TS_ERR_CUDA; }
+        if (h->r_recv.nch) { launch_restrict(a, h->r_recv.d, h->r_recv.ch, h->r_recv.nch, h->d_stage, c); ++n; if (tick(c, 80)) return TS_ERR_CUDA; }
+        if (h->n_heta2) { launch_copies(a, h->d_heta2, h->n_heta2, false, c); ++n; if (tick(c, 96)) return TS_ERR_CUDA; }
+        if (h->x_halo2) { barrier(h, c); ++n; if (tick(c, 65)) return TS_ERR_CUDA; }
         CK(cudaGetLastError());
         return TS_OK;
     };
+    if (h->merged) {
+        // merged exchange phases (build_merged): one launch per phase, the
+        // received values after the phase barrier
+        if (h->n_mx[0]) { launch_xops(a, h->d_mx[0], h->n_mx[0], s); ++n; if (tick(s, 13 * 16)) return TS_ERR_CUDA; }
+        if (mark(2)) return TS_ERR_CUDA;
+        if (h->mx_bar_eta) { barrier(h, s); ++n; if (tick(s, 64)) return TS_ERR_CUDA; }
+        if (h->n_mx[1]) { launch_xops(a, h->d_mx[1], h->n_mx[1], s); ++n; if (tick(s, 80)) return TS_ERR_CUDA; }
+        if (mark(3)) return TS_ERR_CUDA;
+        if (int rc = march(0, s)) return rc;
+        if (mark(4)) return TS_ERR_CUDA;
+        if (mark(5)) return TS_ERR_CUDA;
+        if (h->n_mx[2]) { launch_xops(a, h->d_mx[2], h->n_mx[2], s); ++n; if (tick(s, 14 * 16)) return TS_ERR_CUDA; }
+        if (mark(6)) return TS_ERR_CUDA;
+        if (h->mx_bar_flux) { barrier(h, s); ++n; if (tick(s, 66)) return TS_ERR_CUDA; }
+        if (h->n_mx[3]) { launch_xops(a, h->d_mx[3], h->n_mx[3], s); ++n; if (tick(s, 176)) return TS_ERR_CUDA; }
+        if (mark(7)) return TS_ERR_CUDA;
+        CK(cudaGetLastError());
+        if (nlaunch) *nlaunch = n;
+        return TS_OK;
+    }
     if (h->overlap) {
         // DESIGN.md §5/§7: the chain and then the march of the tiles that
         // read a cell it writes ("late" tiles: parents' ring lines, ghost
@@ -309,14 +351,14 @@ int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunc
         if (int rc = march(0, s)) return rc;
     }
     if (mark(4)) return TS_ERR_CUDA;
-    if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; }
+    if (h->n_edge) { launch_copies(a, h->d_edge, h->n_edge, h->edge_serial, s); ++n; if (tick(s, 128)) return TS_ERR_CUDA; }
     if (mark(5)) return TS_ERR_CUDA;
-    if (h->p_send.nch) { launch_prolong(a, h->p_send.d, h->p_send.ch, h->p_send.nch, h->d_stage, s); ++n; }
-    if (h->p_local.nch) { launch_prolong(a, h->p_local.d, h->p_local.ch, h->p_local.nch, h->d_stage, s); ++n; }
-    if (h->x_prolong) { barrier(h, s); ++n; }
-    if (h->p_recv.nch) { launch_prolong(a, h->p_recv.d, h->p_recv.ch, h->p_recv.nch, h->d_stage, s); ++n; }
+    if (h->p_send.nch) { launch_prolong(a, h->p_send.d, h->p_send.ch, h->p_send.nch, h->d_stage, s); ++n; if (tick(s, 144)) return TS_ERR_CUDA; }
+    if (h->p_local.nch) { launch_prolong(a, h->p_local.d, h->p_local.ch, h->p_local.nch, h->d_stage, s); ++n; if (tick(s, 160)) return TS_ERR_CUDA; }
+    if (h->x_prolong) { barrier(h, s); ++n; if (tick(s, 66)) return TS_ERR_CUDA; }
+    if (h->p_recv.nch) { launch_prolong(a, h->p_recv.d, h->p_recv.ch, h->p_recv.nch, h->d_stage, s); ++n; if (tick(s, 176)) return TS_ERR_CUDA; }
     if (mark(6)) return TS_ERR_CUDA;
-    if (h->n_hflux) { launch_copies(a, h->d_hflux, h->n_hflux, false, s); ++n; }
+    if (h->n_hflux) { launch_copies(a, h->d_hflux, h->n_hflux, false, s); ++n; if (tick(s, 192)) return TS_ERR_CUDA; }
     // "output" is folded into the next step's K_mass (and the end-of-run
     // flush); the swap is the parity flip of the caller
     if (mark(7)) return TS_ERR_CUDA;
@@ -509,6 +551,240 @@ int upload(Tv **dptr, const std::vector<Tv> &v)
     if (v.empty()) return TS_OK;
     CK(cudaMalloc((void **)dptr, v.size() * sizeof(Tv)));
     CK(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(Tv), cudaMemcpyHostToDevice));
+    return TS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Merged exchange phases.  Each exchange phase of the
+// reference is a sequence of element writes: the eta phase is restriction
+// (every value packed from the phase's input, then applied; coupling.py:
+// 278-315) followed by the halo copies in order (exchange.py:218-275); the
+// flux phase is the edge rules in order (kernels.py:274-306), prolongation
+// (packed, then applied; coupling.py:318-340) and the flux halo copies.
+// Replaying that sequence on the host with every value kept as an
+// expression in the phase's INPUT state (a copy of a cell written earlier in
+// the phase becomes that write's expression) leaves one write per
+// destination whose reads are all phase inputs.  When no read cell is also
+// written (checked), the writes are independent: one launch per phase and
+// rank, each element run by the rank holding its source data.  An element
+// whose destination is another rank's interior cell (which that rank's own
+// kernels write earlier in the step) goes through the receiver's receive
+// area and is applied after the phase barrier; ghost cells are stored
+// straight into the peer's arena.  Phases that do not pass the checks keep
+// the launch-per-stage path.
+struct XExpr {
+    int kind;           // 0 copy, 1 zero, 2 mean9 (eta patch at idx)
+    int blk, arr;
+    int32_t idx;
+};
+struct XWrite {
+    XExpr e;
+    int blk, arr;
+    int32_t idx;
+};
+
+inline long long xkey(int b, int arr, int32_t idx) { return ((long long)b << 34) ^ ((long long)arr << 32) ^ (uint32_t)idx; }
+
+int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_all, const std::vector<Copy> &flux_all)
+{
+    h->merged = false;
+    if (const char *f = getenv("TSUNAMI_B200_MERGED"))
+        if (f[0] == '0') return TS_OK;
+    if (h->overlap) return TS_OK;
+    auto owner = [&](int b) { return d->blocks[b].owner; };
+    auto P_of = [&](int b) { return h->hb[b].P; };
+    // interior cells: written by the owner's own mass (eta) / march (m, n)
+    auto interior = [&](int b, int arr, int32_t idx) {
+        const int P = P_of(b);
+        const int x = idx / P - TS_G, y = idx % P - TS_G;
+        const int ni = d->blocks[b].ni, nj = d->blocks[b].nj;
+        if (arr == 0) return x >= 0 && x < ni && y >= 0 && y < nj;
+        if (arr == 1) return x >= 0 && x <= ni && y >= 0 && y < nj;
+        return x >= 0 && x < ni && y >= 0 && y <= nj;
+    };
+    auto reads = [&](const XExpr &e, std::vector<long long> &out) {
+        out.clear();
+        if (e.kind == 0) out.push_back(xkey(e.blk, e.arr, e.idx));
+        else if (e.kind == 2) {
+            const int P = P_of(e.blk);
+            for (int dy = 0; dy < 3; ++dy)
+                for (int dx = 0; dx < 3; ++dx) out.push_back(xkey(e.blk, 0, e.idx + dx * P + dy));
+        }
+    };
+    struct Phase {
+        std::unordered_map<long long, XExpr> w;    // cell -> its current expression
+        std::vector<XWrite> seq;
+        bool ok = true;
+    };
+    std::vector<long long> rd;
+    auto subst = [&](Phase &ph, const XExpr &e) {
+        if (e.kind != 0) return e;
+        auto it = ph.w.find(xkey(e.blk, e.arr, e.idx));
+        return it == ph.w.end() ? e : it->second;
+    };
+    // a packed stage: every expression against the state before the stage
+    auto packed = [&](Phase &ph, const std::vector<XWrite> &stage) {
+        std::vector<XWrite> v = stage;
+        for (auto &x : v) {
+            if (x.e.kind == 2) {
+                reads(x.e, rd);
+                for (long long k : rd)
+                    if (ph.w.count(k)) ph.ok = false;     // a mean over cells written earlier
+            } else {
+                x.e = subst(ph, x.e);
+            }
+        }
+        for (auto &x : v) {
+            ph.w[xkey(x.blk, x.arr, x.idx)] = x.e;
+            ph.seq.push_back(x);
+        }
+    };
+    auto sequential = [&](Phase &ph, const std::vector<XWrite> &stage) {
+        for (XWrite x : stage) {
+            x.e = subst(ph, x.e);
+            ph.w[xkey(x.blk, x.arr, x.idx)] = x.e;
+            ph.seq.push_back(x);
+        }
+    };
+    auto copies = [&](const std::vector<Copy> &cs) {
+        std::vector<XWrite> v;
+        for (const Copy &c : cs) {
+            const int arr = (c.src_blk >> 28) & 3, sb = c.src_blk & 0x0fffffff;
+            XExpr e = c.src_idx < 0 ? XExpr{1, c.dst_blk, arr, 0} : XExpr{0, sb, arr, c.src_idx};
+            v.push_back(XWrite{e, c.dst_blk, arr, c.dst_idx});
+        }
+        return v;
+    };
+    Phase pe, pf;
+    {
+        std::vector<XWrite> r;
+        for (int k = 0; k < d->n_restrict; ++k) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            const bool ns = sg.side >= TS_SOUTH;
+            for (int p = 0; p < sg.parent_hi - sg.parent_lo; ++p) {
+                const int x0 = ns ? sg.child_lo + 3 * p : sg.ring_start, y0 = ns ? sg.ring_start : sg.child_lo + 3 * p;
+                const int x = ns ? sg.parent_lo + p : sg.parent_line, y = ns ? sg.parent_line : sg.parent_lo + p;
+                r.push_back(XWrite{XExpr{2, sg.child, 0, pidx(P_of(sg.child), x0, y0)}, sg.parent, 0,
+                                   pidx(P_of(sg.parent), x, y)});
+            }
+        }
+        packed(pe, r);
+        sequential(pe, copies(eta_all));
+    }
+    {
+        std::vector<Copy> edges;
+        for (int k = 0; k < d->n_edges; ++k) {
+            const ts_edge &e = d->edges[k];
+            const ts_block_desc &B = d->blocks[e.block];
+            const int P = P_of(e.block);
+            const bool xs = e.side <= TS_EAST;
+            const int arr = xs ? 1 : 2;
+            const int n_edge = xs ? B.ni : B.nj;
+            const int edge = (e.side == TS_WEST || e.side == TS_SOUTH) ? 0 : n_edge;
+            const int inner = (e.side == TS_WEST || e.side == TS_SOUTH) ? 1 : n_edge - 1;
+            for (int a = e.lo; a < e.hi; ++a) {
+                const int dst = xs ? pidx(P, edge, a) : pidx(P, a, edge);
+                const int src = e.kind == TS_REFLECTIVE ? -1 : (xs ? pidx(P, inner, a) : pidx(P, a, inner));
+                edges.push_back(Copy{e.block | (arr << 28), e.block, src, dst});
+            }
+        }
+        sequential(pf, copies(edges));
+        std::vector<XWrite> pr;
+        for (int k = 0; k < d->n_prolong; ++k) {
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            const bool ns = sg.side >= TS_SOUTH;
+            const int arr = ns ? 2 : 1;
+            for (int p = 0; p < sg.parent_hi - sg.parent_lo; ++p) {
+                const int px = ns ? sg.parent_lo + p : sg.parent_face_line, py = ns ? sg.parent_face_line : sg.parent_lo + p;
+                for (int u = 0; u < 3; ++u) {
+                    const int a = sg.child_lo + 3 * p + u;
+                    const int cx = ns ? a : sg.child_face_line, cy = ns ? sg.child_face_line : a;
+                    pr.push_back(XWrite{XExpr{0, sg.parent, arr, pidx(P_of(sg.parent), px, py)}, sg.child, arr,
+                                        pidx(P_of(sg.child), cx, cy)});
+                }
+            }
+        }
+        packed(pf, pr);
+        sequential(pf, copies(flux_all));
+    }
+    // one write per destination (the last), then: no read cell is written
+    auto finish = [&](Phase &ph) {
+        std::unordered_map<long long, size_t> last;
+        for (size_t k = 0; k < ph.seq.size(); ++k) last[xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)] = k;
+        std::vector<XWrite> out;
+        for (size_t k = 0; k < ph.seq.size(); ++k)
+            if (last[xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)] == k) out.push_back(ph.seq[k]);
+        for (auto &x : out) {
+            reads(x.e, rd);
+            for (long long k : rd)
+                if (last.count(k)) ph.ok = false;
+        }
+        ph.seq.swap(out);
+    };
+    finish(pe);
+    finish(pf);
+    if (!pe.ok || !pf.ok) {
+        if (getenv("TSUNAMI_B200_VERBOSE"))
+            fprintf(stderr, "[tsunami_b200] rank %d: exchange phases not mergeable (eta %d, flux %d)\n", h->rank,
+                    (int)pe.ok, (int)pf.ok);
+        return TS_OK;
+    }
+    // receive slots in global order (every rank computes the same), eta
+    // phase first; they must fit the areas sized by the per-segment path
+    std::vector<size_t> cap(h->nranks, 0), cur(h->nranks, 0);
+    {
+        std::vector<size_t> relems(h->nranks, 0);
+        for (int k = 0; k < d->n_restrict; ++k) {
+            const ts_eta_segment &sg = d->restrict_segs[k];
+            if (owner(sg.child) != owner(sg.parent)) relems[owner(sg.parent)] += sg.parent_hi - sg.parent_lo;
+        }
+        for (int k = 0; k < d->n_prolong; ++k) {
+            const ts_flux_segment &sg = d->prolong_segs[k];
+            if (owner(sg.parent) != owner(sg.child)) relems[owner(sg.child)] += 3 * (size_t)(sg.parent_hi - sg.parent_lo);
+        }
+        cap = relems;
+    }
+    std::vector<XOp> lists[4];
+    bool cross[2] = {false, false}, recv_used = false;
+    auto emit = [&](Phase &ph, std::vector<XOp> &src_list, std::vector<XOp> &recv_list, int which) -> bool {
+        // group the elements by kind so warps stay uniform
+        std::stable_sort(ph.seq.begin(), ph.seq.end(), [](const XWrite &a, const XWrite &b) { return a.e.kind > b.e.kind; });
+        for (const XWrite &x : ph.seq) {
+            const int dst_owner = owner(x.blk);
+            const int exec = x.e.kind == 1 ? dst_owner : owner(x.e.blk);
+            const int32_t src = (x.e.kind == 1 ? 0 : x.e.blk) | (x.e.kind << 28);
+            if (exec != dst_owner) cross[which] = true;
+            if (exec != dst_owner && interior(x.blk, x.arr, x.idx)) {
+                if (cur[dst_owner] >= cap[dst_owner]) return false;
+                const int32_t slot = (int32_t)cur[dst_owner]++;
+                recv_used = true;
+                if (exec == h->rank)
+                    src_list.push_back(XOp{src, TS_XDST_RECV | dst_owner | (x.arr << 28), x.e.idx, slot});
+                if (dst_owner == h->rank)
+                    recv_list.push_back(XOp{h->rank | (3 << 28), x.blk | (x.arr << 28), slot, x.idx});
+            } else if (exec == h->rank) {
+                src_list.push_back(XOp{src, x.blk | (x.arr << 28), x.e.idx, x.idx});
+            }
+        }
+        return true;
+    };
+    if (!emit(pe, lists[0], lists[1], 0) || !emit(pf, lists[2], lists[3], 1)) return TS_OK;
+    for (int q = 0; q < 4; ++q) {
+        h->n_mx[q] = (int64_t)lists[q].size();
+        if (int rc = upload(&h->d_mx[q], lists[q])) return rc;
+    }
+    // the eta barrier orders every cross-rank store of the step before the
+    // receivers' march (flux-phase ghost stores included: the receivers
+    // first read them in the next step's march); the flux barrier orders the
+    // received values, and keeps a sender from refilling a receive area
+    // before its owner has applied it
+    h->mx_bar_eta = cross[0] || cross[1];
+    h->mx_bar_flux = recv_used;
+    h->merged = true;
+    if (getenv("TSUNAMI_B200_VERBOSE"))
+        fprintf(stderr, "[tsunami_b200] rank %d: merged exchange: eta %lld + %lld received, flux %lld + %lld "
+                        "received, barriers eta %d flux %d\n", h->rank, (long long)h->n_mx[0], (long long)h->n_mx[1],
+                (long long)h->n_mx[2], (long long)h->n_mx[3], (int)h->mx_bar_eta, (int)h->mx_bar_flux);
     return TS_OK;
 }
 
@@ -941,6 +1217,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
 
     // ---- halo strips (exchange.py:218-275) as deduplicated element copies
+    std::vector<Copy> eta_all, flux_all;          // every rank's, for the merged phases
     {
         std::vector<Copy> eta, flux;
         for (int k = 0; k < d->n_halo; ++k) {
@@ -974,6 +1251,8 @@ int create_impl(const ts_desc *d, ts_handle *h)
         }
         eta = dedup_last(eta);
         flux = dedup_last(flux);
+        eta_all = eta;
+        flux_all = flux;
         // cells a peer's restriction writes (parent ring lines of a child
         // on another rank): a halo copy reading one must follow the
         // received restriction
@@ -1093,6 +1372,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->n_edge = (int64_t)edges.size();
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
+    if (int rc = build_merged(h, d, eta_all, flux_all)) return rc;
     CK(cudaDeviceSynchronize());
     if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
     h->peer_arena.assign(h->nranks, nullptr);
@@ -1275,6 +1555,49 @@ int ts_run(ts_handle *h, int64_t n_steps)
     h->routines[5] = ph[6] * scale;
     h->routines[6] = 0.0;
     h->total = tot / 1e3;
+    return check_error(h);
+}
+
+int ts_trace_step(ts_handle *h, int32_t *labels, float *us, int32_t cap, int32_t *count)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    if (cap < 0 || (cap > 0 && (!labels || !us)) || !count) return fail(TS_ERR_INVALID, "bad trace buffers");
+    CK(cudaSetDevice(h->device));
+    if (int rc = check_error(h)) return rc;
+    if (h->imported != h->nranks - 1)
+        return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
+                    h->rank, h->imported, h->nranks - 1);
+    if (int rc = fill_bathymetry(h)) return rc;
+    while (h->trace_ev.size() < 96) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        h->trace_ev.push_back(e);
+    }
+    h->trace_label.clear();
+    h->tracing = true;
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = enqueue_step(h, h->stream, h->cur, false, nullptr);
+    cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+    h->tracing = false;
+    if (rc) return rc;
+    if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+    cudaGraphExec_t x;
+    CK(cudaGraphInstantiate(&x, g, 0));
+    CK(cudaGraphLaunch(x, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaGraphExecDestroy(x));
+    CK(cudaGraphDestroy(g));
+    h->cur ^= 1;
+    h->steps += 1;
+    const int n = (int)h->trace_label.size() - 1;
+    *count = n;
+    for (int k = 0; k < n && k < cap; ++k) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, h->trace_ev[k], h->trace_ev[k + 1]));
+        labels[k] = h->trace_label[k + 1];
+        us[k] = ms * 1e3f;
+    }
     return check_error(h);
 }
 
@@ -1664,6 +1987,7 @@ void ts_destroy(ts_handle *h)
     if (h->ev_xfork) cudaEventDestroy(h->ev_xfork);
     if (h->ev_xjoin) cudaEventDestroy(h->ev_xjoin);
     cudaFree(h->d_heta2);
+    for (auto *p : h->d_mx) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }

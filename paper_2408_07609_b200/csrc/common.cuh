@@ -55,6 +55,19 @@ struct Copy {
     int32_t src_blk, dst_blk, src_idx, dst_idx;   // src_blk holds arr in bits 28..29
 };
 
+// one element of a merged exchange phase: every write of the
+// phase with its value expressed in the phase's input state, so the phase's
+// elements are independent and run as one launch
+//   src: bits 0..27 block (kind 3: this rank), bits 28..29 kind:
+//        0 copy, 1 zero, 2 mean of the 3x3 eta patch at sidx (restriction),
+//        3 copy of receive-area slot sidx
+//   dst: bits 0..27 block, or (bit 30 set) the rank whose receive-area slot
+//        didx gets the value; bits 28..29 array (0 eta, 1 m, 2 n)
+struct XOp {
+    int32_t src, dst, sidx, didx;
+};
+#define TS_XDST_RECV 0x40000000
+
 #define TS_NO_ERROR 0xffffffffffffffffULL
 
 // first-error key: lexicographic (block order, what, i, j) so atomicMin
@@ -117,6 +130,7 @@ void launch_restrict(const StepArgs &a, const RSeg *segs, const int2 *chunks, in
 void launch_prolong(const StepArgs &a, const PSeg *segs, const int2 *chunks, int nchunks, double *stage,
                     cudaStream_t s);
 void launch_copies(const StepArgs &a, const Copy *c, int64_t n, bool serial, cudaStream_t s);
+void launch_xops(const StepArgs &a, const XOp *ops, int64_t n, cudaStream_t s);
 void launch_cbrt(const double *in, double *out, int64_t n, cudaStream_t s);
 // h_ext of a block from a 1-D depth profile, ghosts edge-replicated
 void launch_h_profile(const DevBlock &B, const double *prof, int axis, cudaStream_t s);

@@ -60,7 +60,16 @@ def first_error(local, group=None):
     (block order, what, i, j) keys, or None.  A numerics failure ranks ahead
     of a runtime failure (block order -1, e.g. a peer that stopped at a phase
     barrier because of it).  All ranks get the same answer."""
+    import torch
     import torch.distributed as dist
+    # the common case (no rank failed) costs one small all-reduce instead of
+    # the pickled all-gather (~1 ms over NCCL, inside every run() call)
+    dev = (torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
+           else torch.device("cpu"))
+    flag = torch.tensor([0 if local is None else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if int(flag.item()) == 0:
+        return None
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, local, group=group)
     keys = [k for k in out if k is not None]
