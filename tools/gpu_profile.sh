@@ -14,3 +14,5 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_march|k_mass" \
     --launch-skip 10 --launch-count 5 -o $O/${TAG}_full python bench.py --steps 2 --warmup 3 --no-cpu \
     > $O/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 600 ncu --set full --clock-control none -k regex:"k_xops" --launch-skip 4 --launch-count 2 \
+    -o $O/${TAG}_xops python bench.py --steps 2 --warmup 3 --no-cpu > $O/${TAG}_ncu_xops.log 2>&1; echo "ncu xops rc=$?"

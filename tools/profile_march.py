@@ -19,6 +19,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 rep, out = sys.argv[1], sys.argv[2]
+cmd = sys.argv[3] if len(sys.argv) > 3 else ("tools/ncu_kernel.sh (ncu --set full --clock-control none --import-source on "
+                                             "-k regex:k_march --launch-skip 4 --launch-count 4 python "
+                                             "tools/profile_step.py --steps 4)")
 
 
 def ncu(*args):
@@ -52,8 +55,8 @@ for r in raw[2:]:
     name = r[col["Kernel Name"]]
     if "k_march" not in name:
         continue
-    m = re.search(r"k_march<(\d+), (\d+), (\d+), (\d+)>", name)
-    k = {"kernel": name.split("(")[0], "template": [int(x) for x in m.groups()]}
+    m = re.search(r"k_march<(\d+), (\d+), (\d+), (\d+)(?:, (\d+))?>", name)
+    k = {"kernel": name.split("(")[0], "template": [int(x) for x in m.groups() if x is not None]}
     for w in want:
         v = r[col[w]].replace(",", "")
         k[w] = float(v) if v else None
@@ -89,7 +92,7 @@ for r in src:
 cells = group_cells()
 tot_cells = tot_dp = tot_inst = tot_t = 0.0
 for k in kernels:
-    W, TPC, MINB, PK = k["template"]
+    W, TPC, MINB, PK = k["template"][:4]
     c = cells.get((2, 1) if PK else (W, 0), 0)
     key = next((n for n in sums if re.sub(r"\(int\)|\(bool\)", "", n).startswith(k["kernel"].replace("void ", ""))
                 or k["kernel"].replace("void ", "").replace(" ", "") in re.sub(r"\(int\)|\(bool\)", "", n).replace(" ", "")), None)
@@ -101,8 +104,7 @@ for k in kernels:
     tot_inst += ti
     tot_t += k["gpu__time_duration.sum"] or 0
 res = {"report": os.path.basename(rep),
-       "command": "tools/ncu_kernel.sh (ncu --set full --clock-control none --import-source on -k regex:k_march "
-                  "--launch-skip 4 --launch-count 4 python tools/profile_step.py --steps 4)",
+       "command": cmd,
        "cells": tot_cells, "thread_inst_per_cell": tot_inst / tot_cells, "dp_thread_inst_per_cell": tot_dp / tot_cells,
        "march_ms_serialised": tot_t, "kernels": kernels}
 with open(out, "w") as f:

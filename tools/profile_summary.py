@@ -31,8 +31,10 @@ with open(os.path.join(PR, f"{rnd}_launches.md"), "w") as f:
     f.write("`ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 3 "
             "--warmup 3 --no-cpu` (tools/gpu_profile.sh): 12 graph steps (3 warm-up, 3 more while the "
             "clock sampler starts, 3 timed, 3 end-to-end) plus the end-of-run accumulator flush of each "
-            "run and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch and "
-            "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group). Cold-cache, serialised per-launch times; the raw list is `" + rnd + "_launches.csv`.\n\n")
+            "run and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch, "
+            "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group) and the two merged "
+            "exchange phases (`k_xops`: restriction + halo-eta, edges + prolongation + halo-flux). "
+            "Cold-cache, serialised per-launch times; the raw list is `" + rnd + "_launches.csv`.\n\n")
     f.write("| kernel | launches | total µs | share | avg µs |\n|---|---|---|---|---|\n")
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         f.write(f"| `{k}` | {cnt[k]} | {v / 1e3:.1f} | {v / S * 100:.1f} % | {v / cnt[k] / 1e3:.1f} |\n")
@@ -67,6 +69,20 @@ json.dump({"command": "tools/gpu_profile.sh: ncu --set full --clock-control none
                       "-k regex:'k_march|k_mass' --launch-skip 10 --launch-count 5 python bench.py --steps 2 "
                       "--warmup 3 --no-cpu", "kernels": kern},
           open(os.path.join(PR, f"{rnd}_ncu_full.json"), "w"), indent=1)
+xrep = os.path.join(G, f"{tag}_xops.ncu-rep")
+if os.path.exists(xrep):
+    raw = subprocess.run(["ncu", "-i", xrep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    xr = list(csv.reader(raw.splitlines()))
+    xo = []
+    for r in xr[2:]:
+        d = dict(zip(xr[0], r))
+        xo.append({k: d[k] for k in ("Kernel Name", "Grid Size", "gpu__time_duration.sum", "dram__bytes_read.sum",
+                                     "dram__bytes_write.sum", "launch__registers_per_thread") if k in d}
+                  | {"units": {k: xr[1][xr[0].index(k)] for k in ("gpu__time_duration.sum", "dram__bytes_read.sum",
+                                                                   "dram__bytes_write.sum") if k in xr[0]}})
+    json.dump({"command": "tools/gpu_profile.sh: ncu --set full -k regex:k_xops --launch-skip 4 --launch-count 2 "
+                          "(one step's eta and flux phases)", "kernels": xo},
+              open(os.path.join(PR, f"{rnd}_xops_ncu.json"), "w"), indent=1)
 shutil.copy(os.path.join(G, f"{tag}_bench.json"), os.path.join(PR, f"{rnd}_bench_n1.json"))
 shutil.copy(os.path.join(G, f"{tag}_ref.json"), os.path.join(PR, f"{rnd}_bench_ref.json"))
 for e in kern:
