@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -585,12 +586,52 @@ struct XWrite {
 
 inline long long xkey(int b, int arr, int32_t idx) { return ((long long)b << 34) ^ ((long long)arr << 32) ^ (uint32_t)idx; }
 
+// open-addressing map from a cell key (>= 0) to a value, sized once
+template <typename V>
+struct FlatMap {
+    std::vector<long long> keys;
+    std::vector<V> vals;
+    size_t mask = 0;
+    void init(size_t n)
+    {
+        size_t cap = 16;
+        while (cap < 2 * n + 16) cap <<= 1;
+        keys.assign(cap, -1);
+        vals.assign(cap, V{});
+        mask = cap - 1;
+    }
+    // block and array mixed, the element index added linearly: a phase's
+    // writes walk rows and strips, so neighbouring keys share cache lines
+    static size_t slot0(long long k)
+    {
+        uint64_t x = (uint64_t)k >> 32;
+        x *= 0xff51afd7ed558ccdULL;
+        x ^= x >> 29;
+        return (size_t)(x + ((uint64_t)k & 0xffffffffULL));
+    }
+    const V *find(long long k) const
+    {
+        for (size_t i = slot0(k) & mask;; i = (i + 1) & mask) {
+            if (keys[i] == k) return &vals[i];
+            if (keys[i] < 0) return nullptr;
+        }
+    }
+    V &operator[](long long k)
+    {
+        size_t i = slot0(k) & mask;
+        while (keys[i] >= 0 && keys[i] != k) i = (i + 1) & mask;
+        keys[i] = k;
+        return vals[i];
+    }
+};
+
 int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_all, const std::vector<Copy> &flux_all)
 {
     h->merged = false;
     if (const char *f = getenv("TSUNAMI_B200_MERGED"))
         if (f[0] == '0') return TS_OK;
     if (h->overlap) return TS_OK;
+    const auto t_start = std::chrono::steady_clock::now();
     auto owner = [&](int b) { return d->blocks[b].owner; };
     auto P_of = [&](int b) { return h->hb[b].P; };
     // interior cells: written by the owner's own mass (eta) / march (m, n)
@@ -612,15 +653,15 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         }
     };
     struct Phase {
-        std::unordered_map<long long, XExpr> w;    // cell -> its current expression
+        FlatMap<XExpr> w;                          // cell -> its current expression
         std::vector<XWrite> seq;
         bool ok = true;
     };
     std::vector<long long> rd;
     auto subst = [&](Phase &ph, const XExpr &e) {
         if (e.kind != 0) return e;
-        auto it = ph.w.find(xkey(e.blk, e.arr, e.idx));
-        return it == ph.w.end() ? e : it->second;
+        const XExpr *it = ph.w.find(xkey(e.blk, e.arr, e.idx));
+        return it ? *it : e;
     };
     // a packed stage: every expression against the state before the stage
     auto packed = [&](Phase &ph, const std::vector<XWrite> &stage) {
@@ -629,7 +670,7 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
             if (x.e.kind == 2) {
                 reads(x.e, rd);
                 for (long long k : rd)
-                    if (ph.w.count(k)) ph.ok = false;     // a mean over cells written earlier
+                    if (ph.w.find(k)) ph.ok = false;      // a mean over cells written earlier
             } else {
                 x.e = subst(ph, x.e);
             }
@@ -656,6 +697,16 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         return v;
     };
     Phase pe, pf;
+    {
+        size_t ne = eta_all.size(), nf = flux_all.size();
+        for (int k = 0; k < d->n_restrict; ++k) ne += std::max(0, d->restrict_segs[k].parent_hi - d->restrict_segs[k].parent_lo);
+        for (int k = 0; k < d->n_prolong; ++k) nf += 3 * (size_t)std::max(0, d->prolong_segs[k].parent_hi - d->prolong_segs[k].parent_lo);
+        for (int k = 0; k < d->n_edges; ++k) nf += (size_t)std::max(0, d->edges[k].hi - d->edges[k].lo);
+        pe.w.init(ne);
+        pe.seq.reserve(ne);
+        pf.w.init(nf);
+        pf.seq.reserve(nf);
+    }
     {
         std::vector<XWrite> r;
         for (int k = 0; k < d->n_restrict; ++k) {
@@ -709,15 +760,17 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
     }
     // one write per destination (the last), then: no read cell is written
     auto finish = [&](Phase &ph) {
-        std::unordered_map<long long, size_t> last;
+        FlatMap<size_t> last;
+        last.init(ph.seq.size());
         for (size_t k = 0; k < ph.seq.size(); ++k) last[xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)] = k;
         std::vector<XWrite> out;
+        out.reserve(ph.seq.size());
         for (size_t k = 0; k < ph.seq.size(); ++k)
-            if (last[xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)] == k) out.push_back(ph.seq[k]);
+            if (*last.find(xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)) == k) out.push_back(ph.seq[k]);
         for (auto &x : out) {
             reads(x.e, rd);
             for (long long k : rd)
-                if (last.count(k)) ph.ok = false;
+                if (last.find(k)) ph.ok = false;
         }
         ph.seq.swap(out);
     };
@@ -783,8 +836,10 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
     h->merged = true;
     if (getenv("TSUNAMI_B200_VERBOSE"))
         fprintf(stderr, "[tsunami_b200] rank %d: merged exchange: eta %lld + %lld received, flux %lld + %lld "
-                        "received, barriers eta %d flux %d\n", h->rank, (long long)h->n_mx[0], (long long)h->n_mx[1],
-                (long long)h->n_mx[2], (long long)h->n_mx[3], (int)h->mx_bar_eta, (int)h->mx_bar_flux);
+                        "received, barriers eta %d flux %d (%.3f s)\n", h->rank, (long long)h->n_mx[0],
+                (long long)h->n_mx[1], (long long)h->n_mx[2], (long long)h->n_mx[3], (int)h->mx_bar_eta,
+                (int)h->mx_bar_flux,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count());
     return TS_OK;
 }
 
@@ -1426,7 +1481,11 @@ int ts_create(const ts_desc *desc, ts_handle **out)
     if (!out) return fail(TS_ERR_INVALID, "null output handle");
     *out = nullptr;
     ts_handle *h = new ts_handle();
+    const auto t0 = std::chrono::steady_clock::now();
     int rc = create_impl(desc, h);
+    if (getenv("TSUNAMI_B200_VERBOSE"))
+        fprintf(stderr, "[tsunami_b200] rank %d: ts_create %.3f s\n", h->rank,
+                std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     if (rc) {
         std::string keep = g_err;
         ts_destroy(h);
