@@ -177,6 +177,7 @@ struct ts_handle {
     bool mx_bar_eta = false, mx_bar_flux = false;
     XOp *d_mx[4] = {};
     int64_t n_mx[4] = {};
+    double *d_mstage = nullptr;           // second-wave staging (recv slot [n_ranks])
     // ts_trace_step: an event after every launch of one captured step
     bool tracing = false;
     std::vector<cudaEvent_t> trace_ev;
@@ -582,6 +583,7 @@ struct XWrite {
     XExpr e;
     int blk, arr;
     int32_t idx;
+    int wave = 0;       // 1: its destination is read by another write of the phase
 };
 
 inline long long xkey(int b, int arr, int32_t idx) { return ((long long)b << 34) ^ ((long long)arr << 32) ^ (uint32_t)idx; }
@@ -656,6 +658,16 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         FlatMap<XExpr> w;                          // cell -> its current expression
         std::vector<XWrite> seq;
         bool ok = true;
+        std::string why;                           // the first check that failed (verbose)
+    };
+    auto cell_str = [&](long long k) {
+        const int b = (int)(k >> 34), arr = (int)((k >> 32) & 3);
+        const int32_t idx = (int32_t)(k & 0xffffffffLL);
+        const int P = P_of(b);
+        char buf[96];
+        snprintf(buf, sizeof buf, "block %d %s (%d, %d)", b, arr == 0 ? "eta" : (arr == 1 ? "m" : "n"),
+                 idx / P - TS_G, idx % P - TS_G);
+        return std::string(buf);
     };
     std::vector<long long> rd;
     auto subst = [&](Phase &ph, const XExpr &e) {
@@ -670,7 +682,10 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
             if (x.e.kind == 2) {
                 reads(x.e, rd);
                 for (long long k : rd)
-                    if (ph.w.find(k)) ph.ok = false;      // a mean over cells written earlier
+                    if (ph.w.find(k) && ph.ok) {          // a mean over cells written earlier
+                        ph.ok = false;
+                        ph.why = "a ring mean reads " + cell_str(k) + ", written earlier in the phase";
+                    }
             } else {
                 x.e = subst(ph, x.e);
             }
@@ -767,10 +782,18 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         out.reserve(ph.seq.size());
         for (size_t k = 0; k < ph.seq.size(); ++k)
             if (*last.find(xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)) == k) out.push_back(ph.seq[k]);
+        // a destination that another write reads (a parent ring cell that a
+        // coarser restriction averages: the reference's packed order reads it
+        // before it is overwritten) is written in a second wave: its value is
+        // computed with the first wave (every read sees the phase's input)
+        // into a staging slot and stored after every read of the phase
+        FlatMap<size_t> pos;
+        pos.init(out.size());
+        for (size_t k = 0; k < out.size(); ++k) pos[xkey(out[k].blk, out[k].arr, out[k].idx)] = k;
         for (auto &x : out) {
             reads(x.e, rd);
             for (long long k : rd)
-                if (last.find(k)) ph.ok = false;
+                if (const size_t *p = pos.find(k)) out[*p].wave = 1;
         }
         ph.seq.swap(out);
     };
@@ -778,8 +801,8 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
     finish(pf);
     if (!pe.ok || !pf.ok) {
         if (getenv("TSUNAMI_B200_VERBOSE"))
-            fprintf(stderr, "[tsunami_b200] rank %d: exchange phases not mergeable (eta %d, flux %d)\n", h->rank,
-                    (int)pe.ok, (int)pf.ok);
+            fprintf(stderr, "[tsunami_b200] rank %d: exchange phases not mergeable (eta: %s; flux: %s)\n", h->rank,
+                    pe.ok ? "ok" : pe.why.c_str(), pf.ok ? "ok" : pf.why.c_str());
         return TS_OK;
     }
     // receive slots in global order (every rank computes the same), eta
@@ -799,6 +822,7 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
     }
     std::vector<XOp> lists[4];
     bool cross[2] = {false, false}, recv_used = false;
+    size_t n_stage = 0;
     auto emit = [&](Phase &ph, std::vector<XOp> &src_list, std::vector<XOp> &recv_list, int which) -> bool {
         // group the elements by kind so warps stay uniform
         std::stable_sort(ph.seq.begin(), ph.seq.end(), [](const XWrite &a, const XWrite &b) { return a.e.kind > b.e.kind; });
@@ -807,8 +831,20 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
             const int exec = x.e.kind == 1 ? dst_owner : owner(x.e.blk);
             const int32_t src = (x.e.kind == 1 ? 0 : x.e.blk) | (x.e.kind << 28);
             if (exec != dst_owner) cross[which] = true;
-            if (exec != dst_owner && interior(x.blk, x.arr, x.idx)) {
-                if (cur[dst_owner] >= cap[dst_owner]) return false;
+            if (x.wave && exec == dst_owner) {
+                // second wave, local: staged, stored with the received values
+                if (exec == h->rank) {
+                    const int32_t slot = (int32_t)n_stage++;
+                    src_list.push_back(XOp{src, TS_XDST_RECV | h->nranks | (x.arr << 28), x.e.idx, slot});
+                    recv_list.push_back(XOp{h->nranks | (3 << 28), x.blk | (x.arr << 28), slot, x.idx});
+                }
+            } else if (exec != dst_owner && (x.wave || interior(x.blk, x.arr, x.idx))) {
+                if (cur[dst_owner] >= cap[dst_owner]) {
+                    if (getenv("TSUNAMI_B200_VERBOSE"))
+                        fprintf(stderr, "[tsunami_b200] rank %d: merged exchange: receive area of rank %d full\n",
+                                h->rank, dst_owner);
+                    return false;
+                }
                 const int32_t slot = (int32_t)cur[dst_owner]++;
                 recv_used = true;
                 if (exec == h->rank)
@@ -822,6 +858,12 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         return true;
     };
     if (!emit(pe, lists[0], lists[1], 0) || !emit(pf, lists[2], lists[3], 1)) return TS_OK;
+    if (n_stage) {
+        CK(cudaMalloc((void **)&h->d_mstage, n_stage * sizeof(double)));
+        h->recv_base[h->nranks] = h->d_mstage;
+        CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->recv_base.size() * sizeof(double *),
+                      cudaMemcpyHostToDevice));
+    }
     for (int q = 0; q < 4; ++q) {
         h->n_mx[q] = (int64_t)lists[q].size();
         if (int rc = upload(&h->d_mx[q], lists[q])) return rc;
@@ -1265,10 +1307,11 @@ int create_impl(const ts_desc *d, ts_handle *h)
             return rc;
     }
     // receive-area bases: own now, peers' as their arenas are mapped
-    h->recv_base.assign(h->nranks, nullptr);
+    // [n_ranks] is this rank's staging of the merged phases' second-wave writes
+    h->recv_base.assign(h->nranks + 1, nullptr);
     if (h->arena) h->recv_base[h->rank] = (double *)(h->arena + h->recv_off[h->rank]);
-    CK(cudaMalloc((void **)&h->d_recv, h->nranks * sizeof(double *)));
-    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->nranks * sizeof(double *), cudaMemcpyHostToDevice));
+    CK(cudaMalloc((void **)&h->d_recv, (h->nranks + 1) * sizeof(double *)));
+    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), (h->nranks + 1) * sizeof(double *), cudaMemcpyHostToDevice));
     if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
 
     // ---- halo strips (exchange.py:218-275) as deduplicated element copies
@@ -2047,6 +2090,7 @@ void ts_destroy(ts_handle *h)
     if (h->ev_xjoin) cudaEventDestroy(h->ev_xjoin);
     cudaFree(h->d_heta2);
     for (auto *p : h->d_mx) cudaFree(p);
+    cudaFree(h->d_mstage);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -2086,7 +2130,7 @@ int ts_ipc_import(ts_handle *h, int32_t peer, const void *in, int64_t len)
     h->peer_arena[peer] = (char *)arena;
     h->peer_sig[peer] = (unsigned long long *)sig;
     h->recv_base[peer] = arena ? (double *)((char *)arena + h->recv_off[peer]) : nullptr;
-    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->nranks * sizeof(double *), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_recv, h->recv_base.data(), h->recv_base.size() * sizeof(double *), cudaMemcpyHostToDevice));
     for (int k = 0; k < h->nb; ++k)
         if (h->desc[k].owner == peer) place_block(h->hb[k], (char *)arena + h->off[k], false);
     CK(cudaMemcpy(h->d_blocks, h->hb.data(), sizeof(DevBlock) * h->nb, cudaMemcpyHostToDevice));

@@ -77,6 +77,39 @@ def test_run_parity(cuda_device, oracle_mod, product, name, nr):
     gpu.close()
 
 
+@pytest.mark.parametrize("name", ("quad_wetdry", "chain", "kochi"))
+def test_per_stage_exchange_path(cuda_device, oracle_mod, product, name, monkeypatch):
+    """TSUNAMI_B200_MERGED=0: every exchange stage as its own launch (the
+    path ts_phase uses) is bitwise the oracle as well."""
+    monkeypatch.setenv("TSUNAMI_B200_MERGED", "0")
+    system, settings, n = systems.make(product, name)
+    plan = _plan(product, system, 2 if system.n_blocks > 1 else 1)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    gpu.run(n, threaded=False)
+    orc.run(n)
+    assert_same(gpu, orc, f"per-stage path after {n} steps")
+    gpu.close()
+
+
+def test_merged_exchange_is_the_default(cuda_device, product, monkeypatch):
+    """Kochi at one GPU: mass, at most four march launches and at most two
+    launches per exchange phase (its writes, then the second-wave writes
+    whose destinations the phase also reads); the per-stage path has more."""
+    system, settings, _ = systems.make(product, "kochi")
+    plan = _plan(product, system, 1)
+    monkeypatch.delenv("TSUNAMI_B200_MERGED", raising=False)
+    merged = product.Simulation(system, settings, plan)
+    merged.run(1, threaded=False)
+    monkeypatch.setenv("TSUNAMI_B200_MERGED", "0")
+    staged = product.Simulation(system, settings, plan)
+    staged.run(1, threaded=False)
+    assert merged.launches_per_step <= 1 + 4 + 2 * 2
+    assert merged.launches_per_step < staged.launches_per_step
+    merged.close()
+    staged.close()
+
+
 def test_cfg5_quarter_scale_window(cuda_device, oracle_mod, product):
     """BASELINE config 5 at 1/4 of its cells (10,000 x 10,000 = 100 M cells
     in 8 strips of 1250 x 10,000), 6 steps, bitwise."""
