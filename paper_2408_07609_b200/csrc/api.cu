@@ -1141,6 +1141,17 @@ int create_impl(const ts_desc *d, ts_handle *h)
             for (int T : {124, 94, 64, 48, 32, 24})
                 if (rows[k] / T / tpc >= want) { gr.T = T; break; }
         }
+        // TSUNAMI_B200_TROWS="W:T,..." (tuning): rows per tile of the plain
+        // W-warp group (W = 1..4; T + 2 a multiple of 3)
+        if (const char *f = getenv("TSUNAMI_B200_TROWS")) {
+            for (const char *q = f; *q;) {
+                int W = 0, T = 0, used = 0;
+                if (sscanf(q, "%d:%d%n", &W, &T, &used) != 2) break;
+                if (W >= 1 && W <= 4 && T >= 4 && (T + 2) % 3 == 0) h->groups[W - 1].T = T;
+                q += used;
+                if (*q == ',') ++q;
+            }
+        }
     } else {
         for (auto &gr : h->groups) gr.T = h->T;
     }
