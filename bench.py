@@ -295,6 +295,10 @@ def run_ours(args):
         sim.run(max(args.warmup, 100), threaded=False)     # >= 0.2 s of load: several samples
         barrier()
         torch.cuda.synchronize()
+        # ranks leave the host barrier up to a few hundred us apart; meeting
+        # on the device right before the start event keeps that skew out of
+        # the max-over-ranks time
+        sim.device_barrier()
         start.record(ext)
         sim.run(args.steps, threaded=False)
         end.record(ext)
@@ -326,6 +330,7 @@ def run_ours(args):
     sim.upload_initial_state(arrays)
     sim.download_outputs(outs)
     barrier()
+    sim.device_barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     sim.reset()

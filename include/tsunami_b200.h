@@ -197,6 +197,10 @@ int64_t ts_steps_done(ts_handle *h);
 int64_t ts_device_bytes(ts_handle *h);
 /* kernels launched per ts_run step (graph nodes) */
 int32_t ts_launches_per_step(ts_handle *h);
+/* enqueue a device barrier of all ranks on the library stream (collective;
+ * no-op on one rank): work enqueued after it starts on every rank within
+ * the barrier's latency, e.g. a timed region's start event */
+int ts_device_barrier(ts_handle *h);
 /* diagnostic: run ONE step (collective across ranks, like ts_run(1) without
  * the end-of-run fold) as a graph with an event after every launch, the
  * width groups' march launches serialised; for launch k, labels[k] = kind * 16

@@ -105,6 +105,7 @@ def lib():
     L.ts_launches_per_step.restype = c_int32
     L.ts_set_timing.argtypes = [c_void_p, c_int32]
     L.ts_trace_step.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_void_p]
+    L.ts_device_barrier.argtypes = [c_void_p]
     L.ts_kernel_seconds.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
     L.ts_stream.argtypes = [c_void_p, ctypes.POINTER(c_void_p)]
     L.ts_destroy.argtypes = [c_void_p]
@@ -126,7 +127,7 @@ def lib():
 
 EXPORTED = ("ts_last_error", "ts_abi_version", "ts_create", "ts_run", "ts_phase", "ts_get_field",
             "ts_set_field", "ts_error_info", "ts_timings", "ts_steps_done", "ts_device_bytes",
-            "ts_launches_per_step", "ts_set_timing", "ts_trace_step", "ts_kernel_seconds", "ts_stream", "ts_destroy",
+            "ts_launches_per_step", "ts_set_timing", "ts_trace_step", "ts_device_barrier", "ts_kernel_seconds", "ts_stream", "ts_destroy",
             "ts_ipc_export", "ts_ipc_import", "ts_cbrt_host", "ts_cbrt_device", "ts_set_initial_eta",
             "ts_host_alloc", "ts_host_free", "ts_reset", "ts_upload_inputs", "ts_download_fields", "ts_upload_profiles")
 

@@ -161,6 +161,9 @@ struct ts_handle {
     cudaGraphExec_t gexec_multi[2] = {};
     cudaGraphNode_t ev_node_multi[2][kPhaseEvents] = {};
     cudaEvent_t ev[kPhaseEvents] = {};
+    cudaEvent_t ev_first[kPhaseEvents] = {};    // the first step of a run (get_graph_first)
+    cudaGraph_t graph_first[2] = {};
+    cudaGraphExec_t gexec_first[2] = {};
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     int cur = 0;
     int64_t steps = 0;
@@ -215,18 +218,19 @@ void barrier(ts_handle *h, cudaStream_t s)
 // The step body, in the reference's phase order (runner.py:352-365).  When
 // `events` the phase boundaries are recorded (external event nodes when
 // captured into a graph).
-int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunch)
+int enqueue_step(ts_handle *h, cudaStream_t s, int cur, bool events, int *nlaunch, cudaEvent_t *evs = nullptr)
 {
     const StepArgs a = args_of(h, cur);
+    if (!evs) evs = h->ev;
     int n = 0;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(s, &cap));
     auto mark = [&](int k) -> int {
         if (!events) return 0;
         if (cap == cudaStreamCaptureStatusActive)
-            CK(cudaEventRecordWithFlags(h->ev[k], s, cudaEventRecordExternal));
+            CK(cudaEventRecordWithFlags(evs[k], s, cudaEventRecordExternal));
         else
-            CK(cudaEventRecord(h->ev[k], s));
+            CK(cudaEventRecord(evs[k], s));
         return 0;
     };
     // ts_trace_step: an external event after every launch, labelled with
@@ -406,6 +410,24 @@ int get_graph(ts_handle *h, int c, cudaGraphExec_t *out)
         h->graph[c] = g;
     }
     *out = h->gexec[c];
+    return TS_OK;
+}
+
+// the first step of a run: phase events of its own (read once the run is
+// done, so the host never waits in the middle of a run)
+int get_graph_first(ts_handle *h, int c, cudaGraphExec_t *out)
+{
+    if (!h->gexec_first[c]) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        int rc = enqueue_step(h, h->stream, c, true, nullptr, h->ev_first);
+        cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+        if (rc) return rc;
+        if (e != cudaSuccess) return fail(TS_ERR_CUDA, "graph capture: %s", cudaGetErrorString(e));
+        CK(cudaGraphInstantiate(&h->gexec_first[c], g, 0));
+        h->graph_first[c] = g;
+    }
+    *out = h->gexec_first[c];
     return TS_OK;
 }
 
@@ -961,6 +983,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
     for (auto &e : h->ev_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto &e : h->ev) CK(cudaEventCreate(&e));
+    for (auto &e : h->ev_first) CK(cudaEventCreate(&e));
     CK(cudaEventCreate(&h->t0));
     CK(cudaEventCreate(&h->t1));
 
@@ -1571,11 +1594,9 @@ int ts_run(ts_handle *h, int64_t n_steps)
     // first step: its phase events apportion the call's device time to the
     // routines (runner.ROUTINES)
     cudaGraphExec_t g;
-    if (int rc = get_graph(h, h->cur, &g)) return rc;
+    if (int rc = get_graph_first(h, h->cur, &g)) return rc;
     CK(cudaGraphLaunch(g, s));
     float ph[7] = {0};
-    CK(cudaEventSynchronize(h->ev[kPhaseEvents - 1]));
-    for (int k = 0; k < 7; ++k) CK(cudaEventElapsedTime(&ph[k], h->ev[k], h->ev[k + 1]));
     h->cur ^= 1;
     h->steps += 1;
     int64_t done = 1;
@@ -1655,6 +1676,7 @@ int ts_run(ts_handle *h, int64_t n_steps)
     CK(cudaStreamSynchronize(s));
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, h->t0, h->t1));
+    for (int k = 0; k < 7; ++k) CK(cudaEventElapsedTime(&ph[k], h->ev_first[k], h->ev_first[k + 1]));
     const double sum = ph[0] + ph[1] + ph[2] + ph[3] + ph[4] + ph[5] + ph[6];
     const double scale = sum > 0 ? (tot / 1e3) / sum : 0.0;
     // ROUTINES order: mass, momentum, restrict, prolong, halo-eta, halo-flux,
@@ -1712,6 +1734,19 @@ int ts_trace_step(ts_handle *h, int32_t *labels, float *us, int32_t cap, int32_t
         us[k] = ms * 1e3f;
     }
     return check_error(h);
+}
+
+int ts_device_barrier(ts_handle *h)
+{
+    if (!h) return fail(TS_ERR_INVALID, "null handle");
+    if (h->nranks < 2) return TS_OK;
+    if (h->imported != h->nranks - 1)
+        return fail(TS_ERR_INVALID, "rank %d: %d of %d peers mapped; call ts_ipc_import for every peer first",
+                    h->rank, h->imported, h->nranks - 1);
+    CK(cudaSetDevice(h->device));
+    barrier(h, h->stream);
+    CK(cudaGetLastError());
+    return TS_OK;
 }
 
 int ts_set_timing(ts_handle *h, int32_t on)
@@ -2048,6 +2083,12 @@ void ts_destroy(ts_handle *h)
         if (g) cudaGraphDestroy(g);
     for (auto &g : h->gexec)
         if (g) cudaGraphExecDestroy(g);
+    for (auto &g : h->gexec_first)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto &g : h->graph_first)
+        if (g) cudaGraphDestroy(g);
+    for (auto &e : h->ev_first)
+        if (e) cudaEventDestroy(e);
     for (auto &g : h->graph)
         if (g) cudaGraphDestroy(g);
     for (auto &gr : h->groups) {

@@ -546,6 +546,12 @@ class Simulation:
             self._raise_numerics(False)
         N.check(rc)
 
+    def device_barrier(self):
+        """All ranks meet on the device, on the library stream (collective;
+        no-op on one rank): what is enqueued next starts within the barrier's
+        latency on every rank."""
+        N.check(N.lib().ts_device_barrier(self._h))
+
     def set_timing(self, on: bool):
         N.check(N.lib().ts_set_timing(self._h, 1 if on else 0))
 
