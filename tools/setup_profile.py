@@ -1,3 +1,9 @@
+"""Where Simulation() setup time goes on Kochi-1.0 (one GPU): cProfile of the
+constructor, plus the library's own ts_create / merged-exchange timings
+(TSUNAMI_B200_VERBOSE).
+
+    python tools/setup_profile.py
+"""
 import cProfile, pstats, os, sys, time
 sys.path.insert(0, os.getcwd())
 os.environ["TSUNAMI_B200_VERBOSE"] = "1"
