@@ -29,9 +29,9 @@ shutil.copy(os.path.join(G, f"{tag}_launches.csv"), os.path.join(PR, f"{rnd}_lau
 with open(os.path.join(PR, f"{rnd}_launches.md"), "w") as f:
     f.write(f"# {title} launch list (Kochi-1.0, 47,211,444 cells, 1 B200)\n\n")
     f.write("`ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --steps 3 "
-            "--warmup 3 --no-cpu` (tools/gpu_profile.sh): 12 graph steps (3 warm-up, 3 more while the "
-            "clock sampler starts, 3 timed, 3 end-to-end) plus the end-of-run accumulator flush of each "
-            "run and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch, "
+            "--warmup 3 --no-cpu` (tools/gpu_profile.sh " + tag + "): 109 steps per kernel (3 warm-up, "
+            "100 more inside the clock sampler's window, 3 timed, 3 end-to-end) plus the end-of-run "
+            "accumulator fold of each run (`k_mass<1, 0>`) and the end-to-end leg's host-transfer repitch kernels.  Per step: one mass launch, "
             "four march launches (width groups W = 2, 1, 3 and the packed nj = 36 group) and the two merged "
             "exchange phases (`k_xops`: restriction + halo-eta, edges + prolongation + halo-flux). "
             "Cold-cache, serialised per-launch times; the raw list is `" + rnd + "_launches.csv`.\n\n")
