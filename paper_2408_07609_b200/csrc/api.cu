@@ -181,6 +181,8 @@ struct ts_handle {
     XOp *d_mx[4] = {};
     int64_t n_mx[4] = {};
     double *d_mstage = nullptr;           // second-wave staging (recv slot [n_ranks])
+    // per owned block: its 1-D depth profile on the device (DevBlock.hprof)
+    std::vector<double *> hprof_buf;
     // ts_trace_step: an event after every launch of one captured step
     bool tracing = false;
     std::vector<cudaEvent_t> trace_ev;
@@ -992,6 +994,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     // the peer's arena is mapped (ts_ipc_import)
     h->desc.assign(d->blocks, d->blocks + d->n_blocks);
     h->hb.assign(h->nb, DevBlock{});
+    h->hprof_buf.assign(h->nb, nullptr);
     h->off.assign(h->nb, 0);
     std::vector<size_t> owner_total(h->nranks, 0);
     for (int b = 0; b < h->nb; ++b) {
@@ -1062,14 +1065,18 @@ int create_impl(const ts_desc *d, ts_handle *h)
             CK(cudaMemcpy2D(B.h, P * 8, bd.h_ext, (size_t)(bd.nj + 4) * 8, (size_t)(bd.nj + 4) * 8,
                             bd.ni + 4, cudaMemcpyHostToDevice));
         } else {
+            // the profile stays on the device: the mass kernel reads it
+            // instead of the interior of h
             const int len = bd.h_axis == 0 ? bd.ni : bd.nj;
             double *prof = nullptr;
-            CK(cudaMalloc((void **)&prof, (size_t)len * 8));
+            CK(cudaMalloc((void **)&prof, (size_t)std::max(bd.ni, bd.nj) * 8));
             CK(cudaMemcpy(prof, bd.h_profile, (size_t)len * 8, cudaMemcpyHostToDevice));
             launch_h_profile(B, prof, bd.h_axis, h->stream);
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(h->stream));
-            CK(cudaFree(prof));
+            h->hprof_buf[b] = prof;
+            B.hprof = prof;
+            B.haxis = bd.h_axis;
             h->h_fill_pending = true;
         }
         if (B.nman)
@@ -1518,6 +1525,22 @@ int create_impl(const ts_desc *d, ts_handle *h)
     return get_graph(h, 0, &g);
 }
 
+// one block's entry of the device table after a host-side change (ordered
+// with the library stream's kernels)
+int push_block_entry(ts_handle *h, int b)
+{
+    CK(cudaMemcpyAsync(h->d_blocks + b, &h->hb[b], sizeof(DevBlock), cudaMemcpyHostToDevice, h->stream));
+    return TS_OK;
+}
+
+// a host write of a block's h_ext: its interior is no longer a 1-D profile
+int drop_profile(ts_handle *h, int b)
+{
+    if (!h->hb[b].hprof) return TS_OK;
+    h->hb[b].hprof = nullptr;
+    return push_block_entry(h, b);
+}
+
 // the siblings' bathymetry strips of device-built h_ext, once, before the
 // first step (peer arenas are mapped by then; the first step's halo-eta
 // barrier orders them before any rank's momentum reads ghost h)
@@ -1810,6 +1833,8 @@ int ts_get_field(ts_handle *h, int32_t block, int32_t field, double *out, int64_
     if (int rc = field_geom(h, block, field, &g)) return rc;
     if (len != (int64_t)g.rows * g.cols) return fail(TS_ERR_INVALID, "length %lld != %d x %d", (long long)len, g.rows, g.cols);
     CK(cudaSetDevice(h->device));
+    if (field == TS_H_EXT)
+        if (int rc = drop_profile(h, block)) return rc;
     if (int rc = io_reserve(h, (size_t)len)) return rc;
     launch_repitch(h->d_io, g.cols, g.ptr, g.pitch, g.rows, g.cols, h->stream);
     CK(cudaGetLastError());
@@ -1945,6 +1970,7 @@ int ts_upload_inputs(ts_handle *h, int32_t n, const int32_t *blocks, const doubl
         const size_t he = h_ext[k] ? (size_t)(B.ni + 4) * (B.nj + 4) : 0, ee = (size_t)B.ni * B.nj;
         double *sh = h->d_bulk + off, *se = sh + he;
         if (he) {                          // (NULL: bathymetry left as is, e.g. ts_upload_profiles)
+            if (int rc = drop_profile(h, blocks[k])) return rc;
             CK(cudaMemcpyAsync(sh, h_ext[k], he * 8, cudaMemcpyHostToDevice, h->stream));
             jobs.push_back(Repitch{B.h, sh, B.P, B.nj + 4, B.ni + 4, B.nj + 4});
         }
@@ -1974,14 +2000,17 @@ int ts_upload_profiles(ts_handle *h, int32_t n, const int32_t *blocks, const dou
         const DevBlock &B = h->hb[blocks[k]];
         total += axes[k] == 0 ? B.ni : B.nj;
     }
-    if (int rc = bulk_reserve(h, total, 0)) return rc;
-    size_t off = 0;
+    (void)total;
     for (int k = 0; k < n; ++k) {
-        const DevBlock &B = h->hb[blocks[k]];
+        const int b = blocks[k];
+        DevBlock &B = h->hb[b];
         const size_t len = axes[k] == 0 ? B.ni : B.nj;
-        CK(cudaMemcpyAsync(h->d_bulk + off, profiles[k], len * 8, cudaMemcpyHostToDevice, h->stream));
-        launch_h_profile(B, h->d_bulk + off, axes[k], h->stream);
-        off += len;
+        if (!h->hprof_buf[b]) CK(cudaMalloc((void **)&h->hprof_buf[b], (size_t)std::max(B.ni, B.nj) * 8));
+        CK(cudaMemcpyAsync(h->hprof_buf[b], profiles[k], len * 8, cudaMemcpyHostToDevice, h->stream));
+        launch_h_profile(B, h->hprof_buf[b], axes[k], h->stream);
+        B.hprof = h->hprof_buf[b];
+        B.haxis = axes[k];
+        if (int rc = push_block_entry(h, b)) return rc;
     }
     CK(cudaGetLastError());
     // the siblings' strips (exchange.py:281-300), once every rank's
@@ -2143,6 +2172,7 @@ void ts_destroy(ts_handle *h)
     cudaFree(h->d_heta2);
     for (auto *p : h->d_mx) cudaFree(p);
     cudaFree(h->d_mstage);
+    for (double *p : h->hprof_buf) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }

@@ -23,6 +23,10 @@ struct DevBlock {
     double kf;                      // ((dt*grav)*n)*n, scalar n    (kernels.py:240)
     double dtg;                     // dt * grav
     int32_t has_nman, pad;
+    // interior bathymetry as its 1-D depth profile (h = hprof[haxis ? j : i]),
+    // or null: the mass kernel then reads ni or nj doubles instead of ni x nj
+    const double *hprof;
+    int32_t haxis, pad2;
 };
 
 // one unit of the march kernels: face rows [i0, i1) x output columns

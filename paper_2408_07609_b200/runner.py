@@ -258,13 +258,16 @@ class DeviceBlockState:
         return {"eta": (ni + 4, nj + 4), "m_o": (ni + 5, nj + 4), "n_o": (ni + 4, nj + 5),
                 "m_n": (ni + 5, nj + 4), "n_n": (ni + 4, nj + 5), "h_e": (ni + 4, nj + 4)}[name[:3]]
 
-    def _get(self, name):
+    def _get(self, name, hand=True):
+        """``hand``: the caller may edit the mirror in place, so it is pushed
+        back before the next device call (False for reads made here)."""
         if name not in self._mirror:
             arr = np.empty(self._shape(name))
             N.check(N.lib().ts_get_field(self._sim._h, self._index, N.FIELDS[name],
                                          arr.ctypes.data, arr.size))
             self._mirror[name] = arr
-        self._handed.add(name)
+        if hand:
+            self._handed.add(name)
         return self._mirror[name]
 
     eta_old = property(lambda s: s._get("eta_old"))
@@ -281,8 +284,8 @@ class DeviceBlockState:
         the buffer its last writer used (kernels.py:103-105, 155; exchange.py
         :255-257; coupling.py:315) — eta_new within a step, eta_old after the
         step's swap."""
-        eta = self.eta_old if self._sim._wet_role == "old" else self.eta_new
-        return (self.h_ext + eta) >= self._thr
+        eta = self._get("eta_old" if self._sim._wet_role == "old" else "eta_new", hand=False)
+        return (self._get("h_ext", hand=False) + eta) >= self._thr
 
     def interior(self, arr):
         g = self.halo

@@ -263,3 +263,29 @@ def test_end_to_end_with_device_bathymetry(cuda_device, product):
             assert np.array_equal(a.view(np.uint64), b.view(np.uint64)), (bid, f)
     sim.close()
     fresh.close()
+
+
+def test_edited_bathymetry_of_a_profiled_block(cuda_device, oracle_mod, product):
+    """The mass kernel reads a profiled block's depth from its 1-D profile;
+    an in-place edit of h_ext (kernels.py BlockState arrays are writable)
+    must replace it: the run equals the oracle's on the edited depth."""
+    system, settings, _ = systems.kochi(product, 0.001)
+    plan = _plan(product, system, 1)
+    gpu = product.Simulation(system, settings, plan)
+    orc = oracle_mod.OracleSimulation(system, settings, plan)
+    gpu.run(3, threaded=False)
+    orc.run(3)
+    bid = system.all_blocks()[-1][1].block_id
+    for st in (gpu.states[bid], orc.states[bid]):
+        st.h_ext[4, 5] += 7.25
+        st.h_ext[6, 3] *= 0.5
+    gpu.run(6, threaded=False)
+    orc.run(6)
+    for b, o in orc.states.items():
+        g = gpu.states[b]
+        for f in ("eta_old", "m_old", "n_old", "h_ext"):
+            assert np.array_equal(getattr(g, f).view(np.uint64), getattr(o, f).view(np.uint64)), (b, f)
+        for f in ("max_eta", "max_speed", "max_inundation"):
+            a, c = getattr(gpu.accumulators[b], f), getattr(o, f)
+            assert np.array_equal(a.view(np.uint64), np.asarray(c).view(np.uint64)), (b, f)
+    gpu.close()
