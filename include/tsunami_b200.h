@@ -201,8 +201,9 @@ int32_t ts_launches_per_step(ts_handle *h);
  * no-op on one rank): work enqueued after it starts on every rank within
  * the barrier's latency, e.g. a timed region's start event */
 int ts_device_barrier(ts_handle *h);
-/* diagnostic: run ONE step (collective across ranks, like ts_run(1) without
- * the end-of-run fold) as a graph with an event after every launch, the
+/* diagnostic: run ONE step (collective across ranks; the same state as
+ * ts_run(1), end-of-run fold included) as a graph with an event after every
+ * launch, the
  * width groups' march launches serialised; for launch k, labels[k] = kind * 16
  * + group and us[k] = device microseconds since the previous launch ended.
  * Kinds: 0 mass, 1 restrict (sources), 2 restrict (second pass), 3 halo-eta,

@@ -1732,6 +1732,9 @@ int ts_trace_step(ts_handle *h, int32_t *labels, float *us, int32_t cap, int32_t
         h->trace_ev.push_back(e);
     }
     h->trace_label.clear();
+    // as ts_run(1): the step folds nothing of the past (the previous run
+    // ended with its fold) and its own maxima are folded after it
+    CK(cudaMemsetAsync(h->d_accflag, 0, sizeof(int), h->stream));
     h->tracing = true;
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
@@ -1743,6 +1746,7 @@ int ts_trace_step(ts_handle *h, int32_t *labels, float *us, int32_t cap, int32_t
     cudaGraphExec_t x;
     CK(cudaGraphInstantiate(&x, g, 0));
     CK(cudaGraphLaunch(x, h->stream));
+    if (int rc2 = enqueue_flush(h, h->stream, h->cur ^ 1)) return rc2;
     CK(cudaStreamSynchronize(h->stream));
     CK(cudaGraphExecDestroy(x));
     CK(cudaGraphDestroy(g));

@@ -289,3 +289,34 @@ def test_edited_bathymetry_of_a_profiled_block(cuda_device, oracle_mod, product)
             a, c = getattr(gpu.accumulators[b], f), getattr(o, f)
             assert np.array_equal(a.view(np.uint64), np.asarray(c).view(np.uint64)), (b, f)
     gpu.close()
+
+
+def test_trace_step_is_a_step(cuda_device, product):
+    """ts_trace_step (tools/trace_step.py) advances the state exactly as
+    ts_run(1) does, and reports every launch of the step."""
+    import ctypes
+    from paper_2408_07609_b200 import _native as N
+    system, settings, _ = systems.kochi(product, 0.001)
+    plan = _plan(product, system, 1)
+    a = product.Simulation(system, settings, plan)
+    a.run(2, threaded=False)
+    a.run(1, threaded=False)
+    a.run(2, threaded=False)
+    b = product.Simulation(system, settings, plan)
+    b.run(2, threaded=False)
+    lab, us, cnt = (ctypes.c_int32 * 64)(), (ctypes.c_float * 64)(), ctypes.c_int32()
+    N.check(N.lib().ts_trace_step(b._h, lab, us, 64, ctypes.byref(cnt)))
+    b._invalidate()
+    b.steps_done += 1
+    b.run(2, threaded=False)
+    assert cnt.value == b.launches_per_step
+    assert all(us[k] >= 0.0 for k in range(cnt.value))
+    for bid in a.states:
+        for f in ("eta_old", "m_old", "n_old"):
+            assert np.array_equal(getattr(a.states[bid], f).view(np.uint64),
+                                  getattr(b.states[bid], f).view(np.uint64)), (bid, f)
+        for f in ("max_eta", "max_speed", "max_inundation"):
+            assert np.array_equal(getattr(a.accumulators[bid], f).view(np.uint64),
+                                  getattr(b.accumulators[bid], f).view(np.uint64)), (bid, f)
+    a.close()
+    b.close()
