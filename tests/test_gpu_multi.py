@@ -54,3 +54,27 @@ def test_decomposed_run_bitwise_equals_one_gpu(system, scale, steps, plan, ranks
     for out in lines:                     # one line per system (fuzz: per random seed)
         assert out["ranks"] == ranks
         assert out["bitwise_equal_to_1gpu"], (out["system"], out["diffs"][:5])
+
+
+@pytest.mark.parametrize("system,scale,steps,plan", (("kochi", 0.001, 20, "packed"),
+                                                      ("kochi", 0.001, 20, "minmax"),
+                                                      ("fuzz", 0.0, 30, "packed")))
+def test_eight_ranks_on_shared_gpus(system, scale, steps, plan):
+    """Eight ranks (the 8-GPU rank count) on a box with fewer GPUs: the ranks
+    share GPUs round-robin (tools/mgpu_check.py), so the 8-rank exchange
+    tables, receive areas and barriers are checked bitwise against the
+    one-process run."""
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--system", system, "--steps", str(steps),
+           "--plan", plan]
+    cmd += ["--scale", str(scale)] if system == "kochi" else ["--seeds", "24"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    lines = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert lines
+    for out in lines:
+        assert out["ranks"] == 8
+        assert out["bitwise_equal_to_1gpu"], (out["system"], out["diffs"][:5])

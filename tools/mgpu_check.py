@@ -2,6 +2,9 @@
 
     torchrun --standalone --nproc-per-node 2 tools/mgpu_check.py [--system kochi] [--steps 40]
 
+More processes than GPUs share the GPUs round-robin (an 8-rank check runs on
+a 4-GPU box).
+
 Runs the system decomposed over all ranks (blocks -> GPUs by an exact
 min-max or the packed plan, exchanges over NVLink peer stores), gathers
 every block's state on rank 0, runs the same system and plan on rank 0's
@@ -38,6 +41,9 @@ FIELDS = ("eta_old", "eta_new", "m_old", "m_new", "n_old", "n_new")
 ACCS = ("max_eta", "max_speed", "max_inundation")
 
 local = int(os.environ.get("LOCAL_RANK", "0"))
+# more ranks than GPUs (e.g. an 8-rank check on a 4-GPU box): ranks share
+# GPUs round-robin (CUDA IPC works within a device; the contexts time-slice)
+local = local % max(1, torch.cuda.device_count())
 torch.cuda.set_device(local)
 dist.init_process_group("gloo")
 rank, world = dist.get_rank(), dist.get_world_size()
@@ -48,7 +54,7 @@ def check(system, settings, steps, name):
     cells = [b.cell_count for _, b in system.all_blocks()]
     plan = P.minmax_plan(cells, world) if args.plan == "minmax" else P.packed_plan(system, world)
     chunks = (1, steps // 2, steps - 1 - steps // 2)
-    sim = P.Simulation(system, settings, plan, distributed=True)
+    sim = P.Simulation(system, settings, plan, distributed=True, device=local)
     for chunk in chunks:
         sim.run(chunk, threaded=False)
     mine = {bid: {f: getattr(st, f).copy() for f in FIELDS} for bid, st in sim.states.items()}
