@@ -78,3 +78,19 @@ def test_eight_ranks_on_shared_gpus(system, scale, steps, plan):
     for out in lines:
         assert out["ranks"] == 8
         assert out["bitwise_equal_to_1gpu"], (out["system"], out["diffs"][:5])
+
+
+@pytest.mark.parametrize("ranks", (2, 4))
+def test_failure_on_one_rank_stops_every_rank(ranks):
+    """A NaN depth in the last rank's block: every rank raises the same
+    NumericsError as the one-process run (device error words adopted at the
+    phase barriers, agreed on the host), none hangs in a barrier."""
+    if _gpus() < ranks:
+        pytest.skip(f"needs {ranks} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "tools", "mgpu_check.py"), "--system", "nan", "--steps", "6"]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-4000:]
+    out = [json.loads(ln) for ln in res.stdout.splitlines() if ln.startswith("{")][0]
+    assert out["bitwise_equal_to_1gpu"], out

@@ -30,7 +30,8 @@ from paper_2408_07609_b200 import distributed as D  # noqa: E402
 import systems  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--system", default="kochi", help="a systems.py name, kochi, or fuzz (random_nested seeds)")
+ap.add_argument("--system", default="kochi",
+                help="a systems.py name, kochi, fuzz (random_nested seeds), or nan (a failing run)")
 ap.add_argument("--scale", type=float, default=0.001)
 ap.add_argument("--steps", type=int, default=40)
 ap.add_argument("--plan", default="minmax", choices=("minmax", "packed"))
@@ -83,8 +84,42 @@ def check(system, settings, steps, name):
     return ok
 
 
+def check_failure(steps):
+    """A NaN depth on the last rank's block: every rank stops with the same
+    exception and message as the one-process run of the same plan."""
+    blocks = [systems.flat_block(P, k + 1, (80.0 * k, 0.0), 8, 8, 30.0) for k in range(world - 1)]
+    blocks.append(P.Block(world, (80.0 * (world - 1), 0.0), 8, 8, np.where(np.eye(8, dtype=bool), np.nan, 30.0)))
+    system = P.NestedGridSystem(levels=[P.GridLevel(1, 10.0, blocks)])
+    settings = P.SimulationConfig(dt=0.2)
+    plan = P.equal_cell_plan([b.cell_count for _, b in system.all_blocks()], world)
+
+    def outcome(sim):
+        try:
+            sim.run(steps, threaded=False)
+            return ("ok", "")
+        except Exception as exc:          # noqa: BLE001 - the type is the result
+            return (type(exc).__name__, str(exc))
+
+    sim = P.Simulation(system, settings, plan, distributed=True, device=local)
+    mine = outcome(sim)
+    sim.close()
+    outs = [None] * world
+    dist.all_gather_object(outs, mine)
+    ok = True
+    if rank == 0:
+        ref = P.Simulation(system, settings, plan, distributed=False, device=local)
+        want = outcome(ref)
+        ref.close()
+        ok = want[0] == "NumericsError" and all(o == want for o in outs)
+        print(json.dumps({"system": "nan_last_rank", "ranks": world, "steps": steps, "one_process": want,
+                          "ranks_raised": outs, "bitwise_equal_to_1gpu": ok, "diffs": []}), flush=True)
+    return ok
+
+
 ok = True
-if args.system == "kochi":
+if args.system == "nan":
+    ok = check_failure(args.steps)
+elif args.system == "kochi":
     system, settings, _ = systems.kochi(P, args.scale)
     ok = check(system, settings, args.steps, "kochi")
 elif args.system == "fuzz":
