@@ -612,8 +612,11 @@ struct XWrite {
 
 inline long long xkey(int b, int arr, int32_t idx) { return ((long long)b << 34) ^ ((long long)arr << 32) ^ (uint32_t)idx; }
 
-// open-addressing map from a cell key (>= 0) to a value, sized once
-template <typename V>
+// open-addressing map from a cell key (>= 0) to a value, sized once.
+// LOCAL: for xkey layouts (block and array above bit 32, the element index
+// below) the index is added linearly, so a phase's writes, which walk rows
+// and strips, probe neighbouring slots; otherwise a full 64-bit mix
+template <typename V, bool LOCAL = false>
 struct FlatMap {
     std::vector<long long> keys;
     std::vector<V> vals;
@@ -626,14 +629,21 @@ struct FlatMap {
         vals.assign(cap, V{});
         mask = cap - 1;
     }
-    // block and array mixed, the element index added linearly: a phase's
-    // writes walk rows and strips, so neighbouring keys share cache lines
     static size_t slot0(long long k)
     {
-        uint64_t x = (uint64_t)k >> 32;
+        if (LOCAL) {
+            uint64_t y = (uint64_t)k >> 32;
+            y *= 0xff51afd7ed558ccdULL;
+            y ^= y >> 29;
+            return (size_t)(y + ((uint64_t)k & 0xffffffffULL));
+        }
+        uint64_t x = (uint64_t)k;
+        x ^= x >> 33;
         x *= 0xff51afd7ed558ccdULL;
-        x ^= x >> 29;
-        return (size_t)(x + ((uint64_t)k & 0xffffffffULL));
+        x ^= x >> 33;
+        x *= 0xc4ceb9fe1a85ec53ULL;
+        x ^= x >> 33;
+        return (size_t)x;
     }
     const V *find(long long k) const
     {
@@ -679,7 +689,7 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         }
     };
     struct Phase {
-        FlatMap<XExpr> w;                          // cell -> its current expression
+        FlatMap<XExpr, true> w;                    // cell -> its current expression
         std::vector<XWrite> seq;
         bool ok = true;
         std::string why;                           // the first check that failed (verbose)
@@ -799,7 +809,7 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
     }
     // one write per destination (the last), then: no read cell is written
     auto finish = [&](Phase &ph) {
-        FlatMap<size_t> last;
+        FlatMap<size_t, true> last;
         last.init(ph.seq.size());
         for (size_t k = 0; k < ph.seq.size(); ++k) last[xkey(ph.seq[k].blk, ph.seq[k].arr, ph.seq[k].idx)] = k;
         std::vector<XWrite> out;
@@ -811,7 +821,7 @@ int build_merged(ts_handle *h, const ts_desc *d, const std::vector<Copy> &eta_al
         // before it is overwritten) is written in a second wave: its value is
         // computed with the first wave (every read sees the phase's input)
         // into a staging slot and stored after every read of the phase
-        FlatMap<size_t> pos;
+        FlatMap<size_t, true> pos;
         pos.init(out.size());
         for (size_t k = 0; k < out.size(); ++k) pos[xkey(out[k].blk, out[k].arr, out[k].idx)] = k;
         for (auto &x : out) {
@@ -950,6 +960,15 @@ void place_block(DevBlock &B, char *p, bool with_nman)
 
 int create_impl(const ts_desc *d, ts_handle *h)
 {
+    // TSUNAMI_B200_VERBOSE: seconds spent in each part of the setup
+    const bool verbose = getenv("TSUNAMI_B200_VERBOSE") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto setup_mark = [&](const char *what) {
+        if (!verbose) return;
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[tsunami_b200] setup: %s %.3f s\n", what, std::chrono::duration<double>(t - t_prev).count());
+        t_prev = t;
+    };
     if (!d) return fail(TS_ERR_INVALID, "null descriptor");
     if (d->abi_version != TS_ABI_VERSION)
         return fail(TS_ERR_INVALID, "ABI version %d, library is %d", d->abi_version, TS_ABI_VERSION);
@@ -989,6 +1008,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaEventCreate(&h->t0));
     CK(cudaEventCreate(&h->t1));
 
+    setup_mark("start");
     // ---- arena: every rank computes the same per-owner layout for ALL
     // blocks, so a peer block's arrays are (peer arena base + offset) once
     // the peer's arena is mapped (ts_ipc_import)
@@ -1109,6 +1129,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMalloc((void **)&h->d_accflag, sizeof(int)));
     CK(cudaMemset(h->d_accflag, 0, sizeof(int)));
 
+    setup_mark("arena+upload");
     // ---- march tiles: faces [0, ni+1) x N faces [0, nj+1)
     for (int k = 0; k < 4; ++k) h->groups[k].W = k + 1;
     auto width_group = [](int nj, int &W, int &w) {
@@ -1224,6 +1245,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     auto check_blk = [&](int b) { return b >= 0 && b < h->nb; };
     size_t stage_len = 0;
 
+    setup_mark("tiles");
     // ---- coupling segments (coupling.py:278-340).  Pass 1 validates,
     // flags cross-rank traffic and detects whether any written element is
     // also read in the same exchange (then the reference's pack-all-then-
@@ -1272,7 +1294,15 @@ int create_impl(const ts_desc *d, ts_handle *h)
         return up(recv, vr);
     };
     {
-        std::unordered_set<long long> written, read;
+        // two-pass detection: a restricted parent cell that another segment
+        // reads (written cells in an open-addressing set, reads looked up)
+        size_t nw = 0;
+        for (int k = 0; k < d->n_restrict; ++k)
+            nw += (size_t)std::max(0, d->restrict_segs[k].parent_hi - d->restrict_segs[k].parent_lo);
+        FlatMap<char> written;
+        written.init(nw);
+        std::vector<long long> read;
+        read.reserve(9 * nw);
         auto key = [](int b, int x, int y) { return ((long long)b << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8); };
         for (int k = 0; k < d->n_restrict; ++k) {
             const ts_eta_segment &sg = d->restrict_segs[k];
@@ -1285,17 +1315,17 @@ int create_impl(const ts_desc *d, ts_handle *h)
             const bool ns = sg.side >= TS_SOUTH;
             if (d->blocks[sg.child].owner != d->blocks[sg.parent].owner) h->x_restrict = true;
             for (int p = 0; p < count; ++p) {
-                written.insert(key(sg.parent, ns ? sg.parent_lo + p : sg.parent_line, ns ? sg.parent_line : sg.parent_lo + p));
+                written[key(sg.parent, ns ? sg.parent_lo + p : sg.parent_line, ns ? sg.parent_line : sg.parent_lo + p)] = 1;
                 for (int u = 0; u < 3; ++u)
                     for (int v = 0; v < 3; ++v) {
                         const int x = ns ? sg.child_lo + 3 * p + u : sg.ring_start + u;
                         const int y = ns ? sg.ring_start + v : sg.child_lo + 3 * p + v;
-                        read.insert(key(sg.child, x, y));
+                        read.push_back(key(sg.child, x, y));
                     }
             }
         }
-        for (long long w : written)
-            if (read.count(w)) { h->r_two_pass = true; break; }
+        for (long long r : read)
+            if (written.find(r)) { h->r_two_pass = true; break; }
         auto make = [&](int k, int mode, int srank, int64_t first) {
             const ts_eta_segment &sg = d->restrict_segs[k];
             return RSeg{sg.child, sg.parent, sg.side >= TS_SOUTH, sg.child_lo, sg.ring_start, sg.parent_line,
@@ -1309,7 +1339,13 @@ int create_impl(const ts_desc *d, ts_handle *h)
             return rc;
     }
     {
-        std::unordered_set<long long> written, read;
+        size_t nw = 0;
+        for (int k = 0; k < d->n_prolong; ++k)
+            nw += 3 * (size_t)std::max(0, d->prolong_segs[k].parent_hi - d->prolong_segs[k].parent_lo);
+        FlatMap<char> written;
+        written.init(nw);
+        std::vector<long long> read;
+        read.reserve(nw / 3 + 1);
         auto key = [](int b, int arr, int x, int y) {
             return ((long long)b << 44) ^ ((long long)arr << 42) ^ ((long long)(x + 8) << 21) ^ (long long)(y + 8);
         };
@@ -1325,16 +1361,16 @@ int create_impl(const ts_desc *d, ts_handle *h)
             if (d->blocks[sg.child].owner != d->blocks[sg.parent].owner) h->x_prolong = true;
             const int arr = ns ? 2 : 1;
             for (int p = 0; p < count; ++p) {
-                read.insert(key(sg.parent, arr, ns ? sg.parent_lo + p : sg.parent_face_line,
-                                ns ? sg.parent_face_line : sg.parent_lo + p));
+                read.push_back(key(sg.parent, arr, ns ? sg.parent_lo + p : sg.parent_face_line,
+                                   ns ? sg.parent_face_line : sg.parent_lo + p));
                 for (int u = 0; u < 3; ++u) {
                     const int a = sg.child_lo + 3 * p + u;
-                    written.insert(key(sg.child, arr, ns ? a : sg.child_face_line, ns ? sg.child_face_line : a));
+                    written[key(sg.child, arr, ns ? a : sg.child_face_line, ns ? sg.child_face_line : a)] = 1;
                 }
             }
         }
-        for (long long w : written)
-            if (read.count(w)) { h->p_two_pass = true; break; }
+        for (long long r : read)
+            if (written.find(r)) { h->p_two_pass = true; break; }
         auto make = [&](int k, int mode, int srank, int64_t first) {
             const ts_flux_segment &sg = d->prolong_segs[k];
             return PSeg{sg.parent, sg.child, sg.side >= TS_SOUTH, sg.child_lo, sg.child_face_line,
@@ -1355,6 +1391,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_recv, h->recv_base.data(), (h->nranks + 1) * sizeof(double *), cudaMemcpyHostToDevice));
     if (stage_len) CK(cudaMalloc((void **)&h->d_stage, stage_len * sizeof(double)));
 
+    setup_mark("coupling");
     // ---- halo strips (exchange.py:218-275) as deduplicated element copies
     std::vector<Copy> eta_all, flux_all;          // every rank's, for the merged phases
     {
@@ -1476,6 +1513,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
         }
         if (int rc = upload(&h->d_hflux, flux_own)) return rc;
     }
+    setup_mark("halos");
     // ---- outer-boundary edges (kernels.py:274-306)
     {
         std::vector<Copy> edges;
@@ -1511,6 +1549,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
         h->n_edge = (int64_t)edges.size();
         if (int rc = upload(&h->d_edge, edges)) return rc;
     }
+    setup_mark("edges");
     if (int rc = build_merged(h, d, eta_all, flux_all)) return rc;
     CK(cudaDeviceSynchronize());
     if (const char *f = getenv("TSUNAMI_B200_MOMPAR")) h->mom_par = f[0] == '1';
@@ -1522,6 +1561,7 @@ int create_impl(const ts_desc *d, ts_handle *h)
     CK(cudaMemcpy(h->d_peer_sig, h->peer_sig.data(), h->nranks * sizeof(unsigned long long *),
                   cudaMemcpyHostToDevice));
     cudaGraphExec_t g;
+    setup_mark("merged");
     return get_graph(h, 0, &g);
 }
 
